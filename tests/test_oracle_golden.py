@@ -1,0 +1,132 @@
+"""Pin the C oracle (oracle/hrpp_oracle.c) to the real reference.
+
+Every fixture under tests/golden/ was produced by running the reference
+package itself (tests/golden/make_golden.py).  CPU only.
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+WAVES = ("primary", "shadow", "reflection")
+SETTINGS = ((6, 0), (3, 0), (4, 2), (7, 1))
+
+
+def obvh(oracle_mod, name):
+    return oracle_mod.OracleBvh.from_dict(load_golden(f"bvh_{name}.npz"))
+
+
+def test_hash_matches_reference(oracle_mod):
+    g = load_golden("hash.npz")
+    for p in range(1, 8):
+        assert np.array_equal(oracle_mod.hash_rays(g["O"], g["D"], p), g["keys"][p - 1])
+        assert np.array_equal(oracle_mod.hash_rays_np(g["O"], g["D"], p), g["keys"][p - 1])
+
+
+def test_hash_nonfinite(oracle_mod):
+    O = np.zeros((2, 3), np.float32)
+    D = np.array([[0, 0, 1], [0, np.nan, 1]], np.float32)
+    assert oracle_mod.hash_rays(O, D, 3) is None
+    D[1, 1] = np.inf
+    assert oracle_mod.hash_rays(O, D, 3) is None
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_trace_batch_matches_reference(oracle_mod, threads):
+    g = load_golden("trace_soup256.npz")
+    b = obvh(oracle_mod, "soup256")
+    n = g["O"].shape[0]
+    c = b.trace_batch(True, g["O"], g["D"], np.zeros(n), np.full(n, np.inf), threads=threads)
+    for k, v in c.items():
+        assert np.array_equal(v, g[f"c_{k}"]), k
+    a = b.trace_batch(False, g["O"], g["D"], np.zeros(n), g["tmax_any"], threads=threads)
+    for k, v in a.items():
+        assert np.array_equal(v, g[f"a_{k}"]), k
+    c7 = b.trace_batch(True, g["O"], g["D"], np.zeros(n), np.full(n, np.inf), start=7)
+    for k, v in c7.items():
+        assert np.array_equal(v, g[f"c7_{k}"]), k
+
+
+def test_trace_axis_aligned_rays(oracle_mod):
+    g = load_golden("trace_strip8.npz")
+    b = obvh(oracle_mod, "strip8")
+    n = g["O"].shape[0]
+    c = b.trace_batch(True, g["O"], g["D"], np.zeros(n), np.full(n, np.inf))
+    for k, v in c.items():
+        assert np.array_equal(v, g[f"c_{k}"]), k
+    a = b.trace_batch(False, g["O"], g["D"], np.zeros(n), np.full(n, 100.0))
+    for k, v in a.items():
+        assert np.array_equal(v, g[f"a_{k}"]), k
+
+
+@pytest.mark.parametrize("p,g_", SETTINGS)
+@pytest.mark.parametrize("mode", ["limit", "live"])
+def test_wave_sequence_matches_reference(oracle_mod, p, g_, mode):
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden(f"wave_{mode}_p{p}_g{g_}.npz")
+    b = obvh(oracle_mod, "spheres")
+    tables = {True: oracle_mod.OracleTable(p, g_, True), False: oracle_mod.OracleTable(p, g_, False)}
+    for w in WAVES:
+        closest = w != "shadow"
+        rc, out, stats = oracle_mod.trace_wave(
+            b, tables[closest], mode, closest, inp[f"{w}_O"], inp[f"{w}_D"], inp[f"{w}_tmin"],
+            inp[f"{w}_tmax"], capture=True)
+        assert rc == 0
+        assert np.array_equal(stats, ref[f"{w}_stats"]), (w, stats, ref[f"{w}_stats"])
+        for k in ("found", "t", "slot", "leaf"):
+            assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
+        if mode == "limit":
+            for k in ("u", "v", "box", "tri", "visited"):
+                if f"{w}_{k}" in ref:
+                    assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
+            log = out["log"]
+            assert np.array_equal(log["cls"], ref[f"{w}_log_cls"])
+            assert np.array_equal(log["eval_box"], ref[f"{w}_log_eval_box"])
+            assert np.array_equal(log["pred_t"], ref[f"{w}_log_pred_t"])
+            assert np.array_equal(log["pred_slot"], ref[f"{w}_log_pred_slot"])
+            assert np.array_equal(out["keys"], ref[f"{w}_log_keys"])
+        assert tables[closest].dump_lines() == list(ref[f"{w}_dump"])
+        e, s, m = tables[closest].info()
+        assert [e, s, m, 16 * e + 4 * s] == list(ref[f"{w}_tstats"])
+
+
+def test_predict_matches_reference(oracle_mod):
+    g = load_golden("predict.npz")
+    b = obvh(oracle_mod, "soup256")
+    O, D = g["O"], g["D"]
+    n = O.shape[0]
+    for pre, closest, go_up in (("c", True, 1), ("a", False, 0)):
+        t = oracle_mod.OracleTable(4, go_up, closest)
+        keys = oracle_mod.hash_rays(O, D, 4)
+        base = b.trace_batch(True, O, D, np.zeros(n), np.full(n, np.inf))
+        lut = b.ancestor_lut(go_up)
+        half = np.arange(n // 2)
+        sel = half[base["found"][half]]
+        t.record_batch(keys[sel], lut[base["leaf"][sel]])
+        assert t.dump_lines() == list(g[f"{pre}_dump"])
+        tmax = np.full(n, np.inf) if closest else np.full(n, 6.0)
+        out = oracle_mod.predict_batch(b, t, closest, keys, O, D, np.zeros(n), tmax)
+        assert np.array_equal(out["cls"], g[f"{pre}_cls"])
+        tp = out["cls"] == 0
+        assert np.array_equal(out["t"][tp], g[f"{pre}_t"][tp])
+        assert np.array_equal(b.tri_ids[out["slot"][tp]], g[f"{pre}_tri_id"][tp])
+        assert np.array_equal(out["leaf"][tp], g[f"{pre}_leaf"][tp])
+        assert np.array_equal(out["box"], g[f"{pre}_box"])
+        assert np.array_equal(out["est"], g[f"{pre}_est"])
+
+
+def test_record_sequence_matches_reference(oracle_mod):
+    g = load_golden("record.npz")
+    t = oracle_mod.OracleTable(6, 0, True)
+    rc, ins = t.record_batch(g["keys"], g["nodes"])
+    assert rc == 0
+    assert np.array_equal(ins, g["inserted"])
+    assert t.dump_lines() == list(g["dump"])
+
+
+def test_capacity(oracle_mod):
+    t = oracle_mod.OracleTable(6, 0, True, max_entries=2)
+    rc, _ = t.record_batch(np.array([1, 2, 1], np.uint64), np.array([0, 0, 5], np.int32))
+    assert rc == 0
+    rc, _ = t.record_batch(np.array([3], np.uint64), np.array([0], np.int32))
+    assert rc == oracle_mod.CAPACITY
