@@ -1,0 +1,665 @@
+// capi.cu -- the extern "C" boundary (include/hrpp_b200.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hrpp_b200.h"
+#include "hrpp_internal.h"
+
+namespace hrpp {
+
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+Workspace::~Workspace() {
+  for (auto& kv : bufs) cudaFree(kv.second.p);
+}
+
+int Workspace::get_raw(const char* name, size_t bytes, void** out) {
+  Buf& b = bufs[name];
+  if (b.bytes < bytes) {
+    if (b.p) HRPP_CK(cudaFree(b.p));
+    b.p = nullptr;
+    size_t nb = bytes + bytes / 4 + 256;
+    HRPP_CK(cudaMalloc(&b.p, nb));
+    b.bytes = nb;
+  }
+  *out = b.p;
+  return 0;
+}
+
+BvhDev::~BvhDev() {
+  cudaFree(nodes);
+  cudaFree(tris);
+  cudaFree(depth);
+  for (auto& kv : anc) cudaFree(kv.second);
+}
+
+__global__ void k_ancestor(const int32_t* __restrict__ parent, int64_t n, int level,
+                           int32_t* lut) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x = (int32_t)i;
+    for (int k = 0; k < level; k++) {  // hrpp/bvh.py:147-149, clamped at the root
+      int32_t up = parent[x];
+      if (up < 0) break;
+      x = up;
+    }
+    lut[i] = x;
+  }
+}
+
+int BvhDev::ancestor_lut(int level, const int32_t** out) {
+  auto it = anc.find(level);
+  if (it != anc.end()) {
+    *out = it->second;
+    return 0;
+  }
+  int32_t *par = nullptr, *lut = nullptr;
+  HRPP_CK(cudaMalloc(&lut, sizeof(int32_t) * n_nodes));
+  HRPP_CK(cudaMalloc(&par, sizeof(int32_t) * n_nodes));
+  HRPP_CK(cudaMemcpy(par, parent_host.data(), sizeof(int32_t) * n_nodes, cudaMemcpyHostToDevice));
+  k_ancestor<<<grid_for(n_nodes, 256, num_sms() * 8), 256>>>(par, n_nodes, level, lut);
+  HRPP_LAUNCHED();
+  HRPP_CK(cudaDeviceSynchronize());
+  HRPP_CK(cudaFree(par));
+  anc[level] = lut;
+  *out = lut;
+  return 0;
+}
+
+static Workspace& global_ws() {
+  static Workspace ws[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return ws[dev & 63];
+}
+
+static bool is_device_ptr(const void* p);
+
+// Host/device pointer staging for one call: every array is checked on its
+// own; host (pageable or pinned) arrays go through the device workspace.
+struct Stager {
+  Workspace& ws;
+  cudaStream_t st;
+  std::vector<std::tuple<void*, const void*, size_t>> back;
+  int k = 0;
+  Stager(Workspace& w, cudaStream_t s) : ws(w), st(s) {}
+  std::string name() { return "stage" + std::to_string(k++); }
+  template <typename T>
+  int in(const T* p, size_t count, const T** out) {
+    if (!p || count == 0 || is_device_ptr(p)) {
+      *out = p;
+      return 0;
+    }
+    T* d;
+    int rc = ws.get(name().c_str(), count, &d);
+    if (rc) return rc;
+    HRPP_CK(cudaMemcpyAsync(d, p, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    *out = d;
+    return 0;
+  }
+  template <typename T>
+  int out(T* p, size_t count, T** dev) {
+    if (!p || count == 0 || is_device_ptr(p)) {
+      *dev = p;
+      return 0;
+    }
+    T* d;
+    int rc = ws.get(name().c_str(), count, &d);
+    if (rc) return rc;
+    back.emplace_back((void*)p, (const void*)d, sizeof(T) * count);
+    *dev = d;
+    return 0;
+  }
+  // scratch when the caller passed NULL but the pipeline needs the array
+  template <typename T>
+  int need(T** p, size_t count) {
+    if (*p) return 0;
+    return ws.get(name().c_str(), count, p);
+  }
+  int finish() {
+    for (auto& b : back)
+      HRPP_CK(cudaMemcpyAsync(std::get<0>(b), std::get<1>(b), std::get<2>(b),
+                              cudaMemcpyDeviceToHost, st));
+    HRPP_CK(cudaStreamSynchronize(st));
+    return 0;
+  }
+};
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static int choose_stack(int height) {
+  if (height + 2 <= 64) return 64;
+  if (height + 2 <= 256) return 256;
+  if (height + 2 <= 512) return 512;
+  return -1;
+}
+
+struct Pinned {
+  long long* p = nullptr;
+  int get() {
+    if (!p) HRPP_CK(cudaMallocHost(&p, sizeof(long long) * 32));
+    return 0;
+  }
+};
+static Pinned g_pinned;
+
+}  // namespace hrpp
+
+using namespace hrpp;
+
+struct hrpp_bvh_s : BvhDev {};
+struct hrpp_table_s : TableDev {};
+
+#define CHECK_ARG(cond, msg)          \
+  do {                                \
+    if (!(cond)) {                    \
+      set_error("%s", msg);           \
+      return HRPP_INVALID_ARG;        \
+    }                                 \
+  } while (0)
+
+extern "C" {
+
+const char* hrpp_last_error(void) { return g_err.c_str(); }
+int hrpp_version(void) { return 1; }
+int64_t hrpp_launch_count(void) { return g_launches.load(); }
+int hrpp_device_count(int* count) {
+  *count = 0;
+  HRPP_CK(cudaGetDeviceCount(count));
+  return HRPP_OK;
+}
+int hrpp_set_live_rounds(int rounds) {
+  CHECK_ARG(rounds >= 0 && rounds < 1000, "live rounds must be in [0, 1000)");
+  g_live_rounds = rounds;
+  return HRPP_OK;
+}
+
+// ---- hash -----------------------------------------------------------------
+
+int hrpp_hash_rays(const float* O, const float* D, int64_t n, int p, uint64_t* keys,
+                   void* stream) {
+  CHECK_ARG(p >= 1 && p <= 7, "precision_bits must be in [1, 7]");
+  CHECK_ARG(n >= 0, "n must be >= 0");
+  if (n == 0) return HRPP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(global_ws(), st);
+  const float *dO, *dD;
+  uint64_t* dk;
+  int* err;
+  int rc;
+  if ((rc = sg.in(O, 3 * n, &dO)) || (rc = sg.in(D, 3 * n, &dD)) || (rc = sg.out(keys, n, &dk)))
+    return rc;
+  if ((rc = global_ws().get("hash_err", 1, &err))) return rc;
+  HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
+  if ((rc = launch_hash(dO, dD, n, p, dk, err, st))) return rc;
+  if ((rc = g_pinned.get())) return rc;
+  HRPP_CK(cudaMemcpyAsync(g_pinned.p, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if ((rc = sg.finish())) return rc;
+  if (*(int*)g_pinned.p) {
+    set_error("non-finite ray component in hash batch");
+    return HRPP_NONFINITE;
+  }
+  return HRPP_OK;
+}
+
+int hrpp_hash_floats(const float* f, int64_t n, int p, uint32_t* out, void* stream) {
+  CHECK_ARG(p >= 1 && p <= 7, "precision_bits must be in [1, 7]");
+  if (n <= 0) return HRPP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(global_ws(), st);
+  const float* df;
+  uint32_t* dout;
+  int* err;
+  int rc;
+  if ((rc = sg.in(f, n, &df)) || (rc = sg.out(out, n, &dout))) return rc;
+  if ((rc = global_ws().get("hashf_err", 1, &err))) return rc;
+  HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
+  if ((rc = launch_hash_floats(df, n, p, dout, err, st))) return rc;
+  if ((rc = g_pinned.get())) return rc;
+  HRPP_CK(cudaMemcpyAsync(g_pinned.p, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if ((rc = sg.finish())) return rc;
+  if (*(int*)g_pinned.p) {
+    set_error("cannot hash non-finite float");
+    return HRPP_NONFINITE;
+  }
+  return HRPP_OK;
+}
+
+// ---- BVH ------------------------------------------------------------------
+
+int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
+                    const int32_t* right, const int8_t* axis, const int32_t* first,
+                    const int32_t* count, const int32_t* parent, const int32_t* depth,
+                    const float* tv0, const float* tv1, const float* tv2,
+                    const int32_t* tri_ids, int64_t n_nodes, int64_t n_tris, int device,
+                    hrpp_bvh_t* out) {
+  (void)tri_ids;
+  CHECK_ARG(n_nodes >= 1 && n_nodes < (1LL << 30), "node count must be in [1, 2^30)");
+  CHECK_ARG(n_tris >= 0 && n_tris < (1LL << 31), "triangle count out of range");
+  HRPP_CK(cudaSetDevice(device));
+  std::vector<DNode> hn(n_nodes);
+  for (int64_t i = 0; i < n_nodes; i++) {
+    DNode& d = hn[i];
+    for (int a = 0; a < 3; a++) {
+      d.bmin[a] = bmin[3 * i + a];
+      d.bmax[a] = bmax[3 * i + a];
+    }
+    if (left[i] < 0) {
+      CHECK_ARG(first[i] >= 0 && count[i] >= 0 && (int64_t)first[i] + count[i] <= n_tris,
+                "leaf triangle range out of bounds");
+      d.a = ~first[i];
+      d.b = count[i];
+    } else {
+      CHECK_ARG(left[i] < n_nodes && right[i] >= 0 && right[i] < n_nodes,
+                "child index out of range");
+      int ax = axis[i] == 1 ? 1 : (axis[i] == 2 ? 2 : 0);
+      d.a = left[i];
+      d.b = (int32_t)((uint32_t)right[i] | ((uint32_t)ax << 30));
+    }
+  }
+  // tree height from the root (stack bound); guards against cycles
+  int height = 0;
+  {
+    std::vector<std::pair<int32_t, int32_t>> stk{{0, 0}};
+    int64_t steps = 0;
+    while (!stk.empty()) {
+      auto [nd, dep] = stk.back();
+      stk.pop_back();
+      CHECK_ARG(++steps <= 2 * n_nodes + 2, "BVH is not a tree");
+      if (dep > height) height = dep;
+      if (left[nd] >= 0) {
+        stk.push_back({left[nd], dep + 1});
+        stk.push_back({right[nd], dep + 1});
+      }
+    }
+  }
+  int stack = choose_stack(height);
+  CHECK_ARG(stack > 0, "BVH deeper than the 512-entry traversal stack");
+  std::vector<DTri> ht(n_tris > 0 ? n_tris : 1);
+  for (int64_t k = 0; k < n_tris; k++) {
+    const float* a = tv0 + 3 * k;
+    const float* b = tv1 + 3 * k;
+    const float* c = tv2 + 3 * k;
+    ht[k].p0 = make_float4(a[0], a[1], a[2], b[0]);
+    ht[k].p1 = make_float4(b[1], b[2], c[0], c[1]);
+    ht[k].p2 = make_float4(c[2], 0.f, 0.f, 0.f);
+  }
+  auto* h = new hrpp_bvh_s();
+  h->device = device;
+  h->n_nodes = n_nodes;
+  h->n_tris = n_tris;
+  h->height = height;
+  h->stack = stack;
+  h->parent_host.assign(parent, parent + n_nodes);
+  bool ok = cudaMalloc(&h->nodes, sizeof(DNode) * n_nodes) == cudaSuccess &&
+            cudaMalloc(&h->tris, sizeof(DTri) * ht.size()) == cudaSuccess &&
+            cudaMalloc(&h->depth, sizeof(int32_t) * n_nodes) == cudaSuccess &&
+            cudaMemcpy(h->nodes, hn.data(), sizeof(DNode) * n_nodes, cudaMemcpyHostToDevice) ==
+                cudaSuccess &&
+            cudaMemcpy(h->tris, ht.data(), sizeof(DTri) * ht.size(), cudaMemcpyHostToDevice) ==
+                cudaSuccess &&
+            cudaMemcpy(h->depth, depth, sizeof(int32_t) * n_nodes, cudaMemcpyHostToDevice) ==
+                cudaSuccess;
+  if (!ok) {
+    set_error("BVH upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+    delete h;
+    return HRPP_CUDA;
+  }
+  *out = h;
+  return HRPP_OK;
+}
+
+int hrpp_bvh_destroy(hrpp_bvh_t bvh) {
+  delete bvh;
+  return HRPP_OK;
+}
+
+int hrpp_bvh_ancestor_lut(hrpp_bvh_t bvh, int go_up_level, int32_t* lut_host) {
+  CHECK_ARG(bvh, "null BVH");
+  CHECK_ARG(go_up_level >= 0, "go_up_level must be >= 0");
+  HRPP_CK(cudaSetDevice(bvh->device));
+  const int32_t* lut;
+  int rc = bvh->ancestor_lut(go_up_level, &lut);
+  if (rc) return rc;
+  HRPP_CK(cudaMemcpy(lut_host, lut, sizeof(int32_t) * bvh->n_nodes, cudaMemcpyDeviceToHost));
+  return HRPP_OK;
+}
+
+// ---- traversal batch --------------------------------------------------------
+
+int hrpp_trace_batch(hrpp_bvh_t bvh, int kind, const float* O, const float* D,
+                     const double* tmin, const double* tmax, int32_t start, int64_t n,
+                     hrpp_wave_out* out, void* stream) {
+  CHECK_ARG(bvh && out, "null argument");
+  CHECK_ARG(kind == HRPP_HIT_ANY || kind == HRPP_CLOSEST_HIT, "bad ray kind");
+  CHECK_ARG(start >= 0 && start < bvh->n_nodes, "start node out of range");
+  CHECK_ARG(n >= 0 && n < (1LL << 31), "ray count out of range");
+  if (n == 0) return HRPP_OK;
+  HRPP_CK(cudaSetDevice(bvh->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool closest = kind == HRPP_CLOSEST_HIT;
+  Stager sg(global_ws(), st);
+  const float *dO, *dD;
+  const double *d0, *d1;
+  TraceOut to;
+  int rc;
+  if ((rc = sg.in(O, 3 * n, &dO)) || (rc = sg.in(D, 3 * n, &dD)) ||
+      (rc = sg.in(tmin, n, &d0)) || (rc = sg.in(tmax, n, &d1)) ||
+      (rc = sg.out(out->found, n, &to.found)) || (rc = sg.out(out->t, n, &to.t)) ||
+      (rc = sg.out(out->slot, n, &to.slot)) || (rc = sg.out(out->leaf, n, &to.leaf)) ||
+      (rc = sg.out(out->box, n, &to.box)) || (rc = sg.out(out->tri, n, &to.tri)) ||
+      (rc = sg.out(out->visited, n, &to.vis)))
+    return rc;
+  if (closest) {
+    if ((rc = sg.out(out->u, n, &to.u)) || (rc = sg.out(out->v, n, &to.v))) return rc;
+  }
+  if ((rc = launch_trace(*bvh, closest, dO, dD, d0, d1, start, n, nullptr, nullptr, to, nullptr,
+                         st)))
+    return rc;
+  return sg.finish();
+}
+
+// ---- table ------------------------------------------------------------------
+
+int hrpp_table_create(int precision, int go_up_level, int kind, int64_t max_entries, int device,
+                      hrpp_table_t* out) {
+  CHECK_ARG(precision >= 1 && precision <= 7, "precision_bits must be in [1, 7]");
+  CHECK_ARG(go_up_level >= 0, "go_up_level must be >= 0");
+  CHECK_ARG(kind == HRPP_HIT_ANY || kind == HRPP_CLOSEST_HIT, "bad ray kind");
+  CHECK_ARG(max_entries >= 0, "max_entries must be >= 0");
+  HRPP_CK(cudaSetDevice(device));
+  auto* t = new hrpp_table_s();
+  t->device = device;
+  t->precision = precision;
+  t->go_up = go_up_level;
+  t->closest = kind == HRPP_CLOSEST_HIT;
+  t->max_entries = max_entries;
+  t->ws.device = device;
+  int rc = t->reserve(0, 0);
+  if (rc) {
+    delete t;
+    return rc;
+  }
+  HRPP_CK(cudaDeviceSynchronize());
+  *out = t;
+  return HRPP_OK;
+}
+
+int hrpp_table_destroy(hrpp_table_t table) {
+  delete table;
+  return HRPP_OK;
+}
+
+int hrpp_table_clear(hrpp_table_t t) {
+  CHECK_ARG(t, "null table");
+  HRPP_CK(cudaSetDevice(t->device));
+  HRPP_CK(cudaMemset(t->meta, 0, sizeof(long long) * 4));
+  if (t->idx_keys)
+    HRPP_CK(cudaMemset(t->idx_keys, 0xFF, sizeof(unsigned long long) * t->idx_cap));
+  t->n_entries = t->stored = t->arena_used = 0;
+  return HRPP_OK;
+}
+
+int hrpp_table_info(hrpp_table_t t, int64_t* entries, int64_t* stored, int64_t* max_len) {
+  CHECK_ARG(t, "null table");
+  HRPP_CK(cudaSetDevice(t->device));
+  *entries = t->n_entries;
+  *stored = t->stored;
+  if (max_len) return table_max_len(*t, max_len);
+  return HRPP_OK;
+}
+
+static int read_meta_and_finish(TableDev& t, int* err, cudaStream_t st, Stager& sg,
+                                unsigned long long* stats_dev) {
+  int rc;
+  if ((rc = g_pinned.get())) return rc;
+  HRPP_CK(cudaMemcpyAsync(g_pinned.p, t.meta, sizeof(long long) * 3, cudaMemcpyDeviceToHost, st));
+  HRPP_CK(cudaMemcpyAsync(g_pinned.p + 3, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (stats_dev)
+    HRPP_CK(cudaMemcpyAsync(g_pinned.p + 4, stats_dev, sizeof(long long) * 16,
+                            cudaMemcpyDeviceToHost, st));
+  if ((rc = sg.finish())) return rc;
+  int e = *(int*)(g_pinned.p + 3);
+  if (e == 0) {
+    t.n_entries = g_pinned.p[0];
+    t.stored = g_pinned.p[1];
+    t.arena_used = g_pinned.p[2];
+  }
+  return 0;
+}
+
+int hrpp_table_record(hrpp_table_t t, const uint64_t* keys, const int32_t* nodes, int64_t n,
+                      uint8_t* inserted, void* stream) {
+  CHECK_ARG(t, "null table");
+  CHECK_ARG(n >= 0 && n < (1LL << 31), "record count out of range");
+  if (n == 0) return HRPP_OK;
+  HRPP_CK(cudaSetDevice(t->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(global_ws(), st);
+  const uint64_t* dk;
+  const int32_t* dn;
+  uint8_t* di;
+  int* err;
+  int rc;
+  if ((rc = sg.in(keys, n, &dk)) || (rc = sg.in(nodes, n, &dn)) ||
+      (rc = sg.out(inserted, n, &di)))
+    return rc;
+  if ((rc = t->ws.get("t_err", 1, &err))) return rc;
+  HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
+  if ((rc = table_record(*t, dk, dn, n, di, err, st))) return rc;
+  if ((rc = read_meta_and_finish(*t, err, st, sg, nullptr))) return rc;
+  int e = *(int*)(g_pinned.p + 3);
+  if (e == 2) {
+    set_error("predictor table reached its cap of %lld entries", (long long)t->max_entries);
+    return HRPP_CAPACITY;
+  }
+  if (e) {
+    set_error("internal error %d in record", e);
+    return HRPP_CUDA;
+  }
+  return HRPP_OK;
+}
+
+int hrpp_table_lookup(hrpp_table_t t, uint64_t key, int32_t* nodes_host, int64_t cap,
+                      int64_t* len_out) {
+  CHECK_ARG(t && len_out, "null argument");
+  HRPP_CK(cudaSetDevice(t->device));
+  return table_lookup1(*t, key, nodes_host, cap, len_out);
+}
+
+int hrpp_table_export(hrpp_table_t t, uint64_t* keys, int64_t* offsets, int32_t* nodes) {
+  CHECK_ARG(t && keys && offsets, "null argument");
+  HRPP_CK(cudaSetDevice(t->device));
+  return table_export(*t, keys, offsets, nodes);
+}
+
+// ---- predict ------------------------------------------------------------------
+
+int hrpp_predict_batch(hrpp_bvh_t bvh, hrpp_table_t t, const uint64_t* keys, const float* O,
+                       const float* D, const double* tmin, const double* tmax, int64_t n,
+                       int8_t* cls, double* tt, int32_t* slot, int32_t* leaf, double* u,
+                       double* v, int64_t* box, int64_t* tri, int64_t* visited, int64_t* est,
+                       void* stream) {
+  CHECK_ARG(bvh && t && cls, "null argument");
+  CHECK_ARG(n >= 0 && n < (1LL << 31), "ray count out of range");
+  if (n == 0) return HRPP_OK;
+  HRPP_CK(cudaSetDevice(bvh->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(global_ws(), st);
+  const uint64_t* dk;
+  const float *dO, *dD;
+  const double *d0, *d1;
+  int8_t* dc;
+  double *dt, *du, *dv;
+  int32_t *ds, *dl;
+  int64_t *db, *dtr, *dvis, *de;
+  int rc;
+  if ((rc = sg.in(keys, n, &dk)) || (rc = sg.in(O, 3 * n, &dO)) || (rc = sg.in(D, 3 * n, &dD)) ||
+      (rc = sg.in(tmin, n, &d0)) || (rc = sg.in(tmax, n, &d1)) || (rc = sg.out(cls, n, &dc)) ||
+      (rc = sg.out(tt, n, &dt)) || (rc = sg.out(slot, n, &ds)) || (rc = sg.out(leaf, n, &dl)) ||
+      (rc = sg.out(u, n, &du)) || (rc = sg.out(v, n, &dv)) || (rc = sg.out(box, n, &db)) ||
+      (rc = sg.out(tri, n, &dtr)) || (rc = sg.out(visited, n, &dvis)) ||
+      (rc = sg.out(est, n, &de)))
+    return rc;
+  if ((rc = predict_batch(*bvh, *t, dk, dO, dD, d0, d1, n, dc, dt, ds, dl, du, dv, db, dtr, dvis,
+                          de, st)))
+    return rc;
+  return sg.finish();
+}
+
+// ---- the wave -----------------------------------------------------------------
+
+int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const float* O,
+                    const float* D, const double* tmin, const double* tmax, int64_t n,
+                    hrpp_wave_out* out, hrpp_outcome_log* log, int64_t* stats, void* stream) {
+  CHECK_ARG(bvh && stats, "null argument");
+  CHECK_ARG(mode >= HRPP_MODE_BASELINE && mode <= HRPP_MODE_LIVE, "bad mode");
+  CHECK_ARG(mode == HRPP_MODE_BASELINE || t, "limit and live modes need a table");
+  CHECK_ARG(!t || mode == HRPP_MODE_BASELINE || t->closest == (closest != 0),
+            "table kind does not match the wave's ray kind");
+  CHECK_ARG(n >= 0 && n < (1LL << 31), "ray count out of range");
+  stats[0] += n;  // hrpp/tracer.py:350 counts the rays before hashing
+  if (n == 0) return HRPP_OK;
+  HRPP_CK(cudaSetDevice(bvh->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  hrpp_wave_out none{};
+  if (!out) out = &none;
+  Workspace& ws = t ? t->ws : global_ws();
+  Stager sg(ws, st);
+  const float *dO, *dD;
+  const double *d0, *d1;
+  int rc;
+  if ((rc = sg.in(O, 3 * n, &dO)) || (rc = sg.in(D, 3 * n, &dD)) || (rc = sg.in(tmin, n, &d0)) ||
+      (rc = sg.in(tmax, n, &d1)))
+    return rc;
+  TraceOut to;
+  uint64_t* keys = nullptr;
+  if ((rc = sg.out(out->found, n, &to.found)) || (rc = sg.out(out->t, n, &to.t)) ||
+      (rc = sg.out(out->slot, n, &to.slot)) || (rc = sg.out(out->leaf, n, &to.leaf)) ||
+      (rc = sg.out(out->keys, n, &keys)))
+    return rc;
+  if (mode != HRPP_MODE_LIVE) {
+    if ((rc = sg.out(out->box, n, &to.box)) || (rc = sg.out(out->tri, n, &to.tri)) ||
+        (rc = sg.out(out->visited, n, &to.vis)))
+      return rc;
+    if (closest && ((rc = sg.out(out->u, n, &to.u)) || (rc = sg.out(out->v, n, &to.v))))
+      return rc;
+  }
+  hrpp_outcome_log lg{};
+  if (log && mode == HRPP_MODE_LIMIT) {
+    if ((rc = sg.out(log->cls, n, &lg.cls)) || (rc = sg.out(log->eval_box, n, &lg.eval_box)) ||
+        (rc = sg.out(log->pred_t, n, &lg.pred_t)) ||
+        (rc = sg.out(log->pred_slot, n, &lg.pred_slot)))
+      return rc;
+  }
+  // arrays the pipeline needs even if the caller did not ask for them
+  if (mode != HRPP_MODE_BASELINE) {
+    if ((rc = sg.need(&keys, n)) || (rc = sg.need(&to.found, n)) || (rc = sg.need(&to.t, n)) ||
+        (rc = sg.need(&to.leaf, n)))
+      return rc;
+    if (mode == HRPP_MODE_LIMIT && (rc = sg.need(&to.box, n))) return rc;
+    if (mode == HRPP_MODE_LIVE && (rc = sg.need(&to.slot, n))) return rc;
+  }
+  int* err;
+  unsigned long long* sdev;
+  if ((rc = ws.get("w_err", 1, &err)) || (rc = ws.get("w_stats", 16, &sdev))) return rc;
+  HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
+  HRPP_CK(cudaMemsetAsync(sdev, 0, sizeof(unsigned long long) * 16, st));
+  if (mode != HRPP_MODE_BASELINE) {
+    if ((rc = launch_hash(dO, dD, n, t->precision, keys, err, st))) return rc;
+  }
+  if (mode != HRPP_MODE_LIVE) {
+    to.sums = sdev + 4;  // baseline_box_tests, baseline_tri_tests (tracer.py:361-362)
+    if ((rc = launch_trace(*bvh, closest != 0, dO, dD, d0, d1, 0, n, nullptr, nullptr, to, err,
+                           st)))
+      return rc;
+  }
+  if (mode != HRPP_MODE_BASELINE) {
+    Consult c;
+    c.live = mode == HRPP_MODE_LIVE;
+    c.O = dO;
+    c.D = dD;
+    c.tmin = d0;
+    c.tmax = d1;
+    c.n = n;
+    c.base_found = to.found;
+    c.base_t = to.t;
+    c.base_leaf = to.leaf;
+    c.base_box = to.box;
+    c.o_found = to.found;
+    c.o_t = to.t;
+    c.o_slot = to.slot;
+    c.o_leaf = to.leaf;
+    c.log_cls = lg.cls;
+    c.log_eval_box = lg.eval_box;
+    c.log_pred_t = lg.pred_t;
+    c.log_pred_slot = lg.pred_slot;
+    if ((rc = run_consult(*bvh, *t, c, keys, sdev, err, st))) return rc;
+    if ((rc = read_meta_and_finish(*t, err, st, sg, sdev))) return rc;
+  } else {
+    if ((rc = g_pinned.get())) return rc;
+    HRPP_CK(cudaMemcpyAsync(g_pinned.p + 3, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HRPP_CK(cudaMemcpyAsync(g_pinned.p + 4, sdev, sizeof(long long) * 16, cudaMemcpyDeviceToHost,
+                            st));
+    if ((rc = sg.finish())) return rc;
+  }
+  const int e = *(int*)(g_pinned.p + 3);
+  const long long* s = g_pinned.p + 4;
+  if (e == 1) {
+    set_error("non-finite ray component in hash batch");
+    return HRPP_NONFINITE;
+  }
+  if (mode == HRPP_MODE_LIMIT || mode == HRPP_MODE_BASELINE) {
+    stats[4] += s[4];  // the baseline sums precede the consult (tracer.py:361-362)
+    stats[5] += s[5];
+  }
+  if (e == 2) {
+    set_error("predictor table reached its cap of %lld entries", (long long)t->max_entries);
+    return HRPP_CAPACITY;
+  }
+  if (e) {
+    set_error("internal error %d in trace_wave", e);
+    return HRPP_CUDA;
+  }
+  for (int k = 1; k < HRPP_STATS_LEN; k++)
+    if (!((mode != HRPP_MODE_LIVE) && (k == 4 || k == 5))) stats[k] += s[k];
+  return HRPP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// hrpp_device.cuh -- device data layout and the bit-exact f64 traversal core.
+//
+// Layout in HBM:
+//   DNode  32 B  {bmin.xyz, a | bmax.xyz, b}: two 16-B loads per visit.
+//          interior: a = left (>= 0), b = right | axis << 30
+//          leaf:     a = ~first (< 0, so the reference's `left < 0` test
+//                    becomes `a < 0`), b = count
+//   DTri   48 B  {v0.xyz v1.x | v1.yz v2.xy | v2.z pad}: three 16-B loads.
+//
+// Arithmetic restates hrpp/kernels.py:23-206 operation by operation in
+// float64.  The whole library is compiled with --fmad=false so no
+// multiply-add is contracted (numba emits none either), and double division
+// is IEEE round-to-nearest, so results are bit-identical to the reference.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hrpp {
+
+struct __align__(16) DNode {
+  float bmin[3];
+  int32_t a;
+  float bmax[3];
+  int32_t b;
+};
+
+struct __align__(16) DTri {
+  float4 p0, p1, p2;
+};
+
+constexpr double kDetEps = 1e-9;          // hrpp/kernels.py:20
+constexpr double kWrongClosestEps = 1e-9; // hrpp/tracer.py:52
+
+struct Hit {
+  bool found;
+  double t;
+  int32_t slot, leaf;
+  double u, v;
+  int32_t boxes, tris;  // per-ray counts are small; widened when stored
+};
+
+__device__ __forceinline__ double recip(double d) {
+  // hrpp/kernels.py:97-99
+  return d != 0.0 ? 1.0 / d : copysign(__longlong_as_double(0x7ff0000000000000LL), d);
+}
+
+__device__ __forceinline__ void load_node(const DNode* __restrict__ nodes, int32_t nd,
+                                          float4& lo, float4& hi) {
+  const float4* p = reinterpret_cast<const float4*>(nodes + nd);
+  lo = __ldg(p);
+  hi = __ldg(p + 1);
+}
+
+// hrpp/kernels.py:23-51 (inclusive slab test; NaN compares are ignored)
+__device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, double ox, double oy,
+                                        double oz, double ivx, double ivy, double ivz, double t0,
+                                        double t1) {
+  double tn = t0, tf = t1, a, b, s;
+  a = ((double)lo.x - ox) * ivx;
+  b = ((double)hi.x - ox) * ivx;
+  if (ivx < 0.0) { s = a; a = b; b = s; }
+  if (a > tn) tn = a;
+  if (b < tf) tf = b;
+  a = ((double)lo.y - oy) * ivy;
+  b = ((double)hi.y - oy) * ivy;
+  if (ivy < 0.0) { s = a; a = b; b = s; }
+  if (a > tn) tn = a;
+  if (b < tf) tf = b;
+  a = ((double)lo.z - oz) * ivz;
+  b = ((double)hi.z - oz) * ivz;
+  if (ivz < 0.0) { s = a; a = b; b = s; }
+  if (a > tn) tn = a;
+  if (b < tf) tf = b;
+  return tn <= tf;
+}
+
+// hrpp/kernels.py:54-86 (Moller-Trumbore, |det| <= 1e-9 rejected)
+__device__ __forceinline__ bool tri_test(const DTri* __restrict__ tris, int32_t k, double ox,
+                                         double oy, double oz, double dx, double dy, double dz,
+                                         double& t, double& u, double& v) {
+  const float4* p = reinterpret_cast<const float4*>(tris + k);
+  float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
+  double ax = q0.x, ay = q0.y, az = q0.z;
+  double e1x = (double)q0.w - ax, e1y = (double)q1.x - ay, e1z = (double)q1.y - az;
+  double e2x = (double)q1.z - ax, e2y = (double)q1.w - ay, e2z = (double)q2.x - az;
+  double px = dy * e2z - dz * e2y;
+  double py = dz * e2x - dx * e2z;
+  double pz = dx * e2y - dy * e2x;
+  double det = e1x * px + e1y * py + e1z * pz;
+  if (fabs(det) <= kDetEps) return false;
+  double inv_det = 1.0 / det;
+  double tx = ox - ax, ty = oy - ay, tz = oz - az;
+  double uu = (tx * px + ty * py + tz * pz) * inv_det;
+  if (uu < 0.0 || uu > 1.0) return false;
+  double qx = ty * e1z - tz * e1y;
+  double qy = tz * e1x - tx * e1z;
+  double qz = tx * e1y - ty * e1x;
+  double vv = (dx * qx + dy * qy + dz * qz) * inv_det;
+  if (vv < 0.0 || uu + vv > 1.0) return false;
+  t = (e2x * qx + e2y * qy + e2z * qz) * inv_det;
+  u = uu;
+  v = vv;
+  return true;
+}
+
+struct Ray {
+  double ox, oy, oz, dx, dy, dz, ivx, ivy, ivz, tmin, tmax;
+};
+
+__device__ __forceinline__ Ray make_ray(const float* __restrict__ O, const float* __restrict__ D,
+                                        const double* __restrict__ tmin,
+                                        const double* __restrict__ tmax, int64_t i) {
+  Ray r;
+  r.ox = O[3 * i]; r.oy = O[3 * i + 1]; r.oz = O[3 * i + 2];
+  r.dx = D[3 * i]; r.dy = D[3 * i + 1]; r.dz = D[3 * i + 2];
+  r.ivx = recip(r.dx); r.ivy = recip(r.dy); r.ivz = recip(r.dz);
+  r.tmin = tmin[i];
+  r.tmax = tmax[i];
+  return r;
+}
+
+// trace_closest / trace_any from `start` (hrpp/kernels.py:89-206).
+// Traversal order: pop, count visit + box test, leaf = slots [first,
+// first+count) in order, interior pushes far then near (near = left iff
+// d[axis] >= 0, so -0.0 goes left).
+template <bool CLOSEST, int STACK>
+__device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
+                                          const DTri* __restrict__ tris, const Ray& r,
+                                          int32_t start) {
+  int32_t stack[STACK];
+  int top = 1;
+  stack[0] = start;
+  Hit h;
+  h.found = false;
+  h.t = CLOSEST ? r.tmax : 0.0;
+  h.slot = -1;
+  h.leaf = -1;
+  h.u = 0.0;
+  h.v = 0.0;
+  h.boxes = 0;
+  h.tris = 0;
+  while (top > 0) {
+    int32_t nd = stack[--top];
+    h.boxes++;
+    float4 lo, hi;
+    load_node(nodes, nd, lo, hi);
+    if (!box_hit(lo, hi, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax))
+      continue;
+    int32_t a = __float_as_int(lo.w);
+    int32_t b = __float_as_int(hi.w);
+    if (a < 0) {
+      int32_t f = ~a, e = f + b;
+      for (int32_t k = f; k < e; k++) {
+        double t, u, v;
+        h.tris++;
+        if (tri_test(tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) && t >= r.tmin &&
+            t <= r.tmax) {
+          if (!CLOSEST) {
+            h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+            return h;
+          }
+          if (!h.found || t < h.t) {
+            h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+          }
+        }
+      }
+    } else {
+      int axis = (uint32_t)b >> 30;
+      int32_t right = b & 0x3FFFFFFF;
+      double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
+      int32_t nearc = dval >= 0.0 ? a : right;
+      int32_t farc = dval >= 0.0 ? right : a;
+      stack[top++] = farc;
+      stack[top++] = nearc;
+    }
+  }
+  return h;
+}
+
+// One step of eval_entry_{closest,any} (hrpp/kernels.py:251-297): fold the
+// subtree result of the next stored node into the running entry result.
+template <bool CLOSEST>
+__device__ __forceinline__ void fold_entry(Hit& acc, const Hit& r) {
+  acc.boxes += r.boxes;
+  acc.tris += r.tris;
+  if (r.found && (!acc.found || (CLOSEST && r.t < acc.t))) {
+    acc.found = true; acc.t = r.t; acc.slot = r.slot; acc.leaf = r.leaf;
+    acc.u = r.u; acc.v = r.v;
+  }
+}
+
+__device__ __forceinline__ Hit empty_entry_result(bool closest) {
+  Hit h;
+  h.found = false;
+  h.t = closest ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
+  h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0; h.boxes = 0; h.tris = 0;
+  return h;
+}
+
+// Predictor table hash index (open addressing, linear probing).
+constexpr unsigned long long kEmptyKey = ~0ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ int32_t index_lookup(const unsigned long long* __restrict__ keys,
+                                                const int32_t* __restrict__ vals, uint64_t mask,
+                                                uint64_t key) {
+  uint64_t h = mix64(key) & mask;
+  for (;;) {
+    unsigned long long k = keys[h];
+    if (k == key) return vals[h];
+    if (k == kEmptyKey) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace hrpp

@@ -1,0 +1,184 @@
+// hrpp_internal.h -- host-side structures shared by the library's .cu files.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "hrpp_device.cuh"
+
+namespace hrpp {
+
+extern std::atomic<int64_t> g_launches;
+void set_error(const char* fmt, ...);
+
+#define HRPP_CK(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      ::hrpp::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #call,                   \
+                        cudaGetErrorString(e_));                                        \
+      return 4;                                                                         \
+    }                                                                                   \
+  } while (0)
+
+#define HRPP_LAUNCHED()                                                                 \
+  do {                                                                                  \
+    ::hrpp::g_launches.fetch_add(1, std::memory_order_relaxed);                         \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess) {                                                            \
+      ::hrpp::set_error("%s:%d: kernel launch -> %s", __FILE__, __LINE__,               \
+                        cudaGetErrorString(e_));                                        \
+      return 4;                                                                         \
+    }                                                                                   \
+  } while (0)
+
+// Grow-only scratch buffers (contents are not preserved across growth).
+struct Workspace {
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  int device = 0;
+  ~Workspace();
+  int get_raw(const char* name, size_t bytes, void** out);
+  template <typename T>
+  int get(const char* name, size_t count, T** out) {
+    void* p = nullptr;
+    int rc = get_raw(name, count * sizeof(T) + 16, &p);
+    *out = static_cast<T*>(p);
+    return rc;
+  }
+};
+
+// Result arrays of a traversal (any pointer may be null = not stored).
+struct TraceOut {
+  uint8_t* found = nullptr;
+  double* t = nullptr;
+  int32_t* slot = nullptr;
+  int32_t* leaf = nullptr;
+  double* u = nullptr;
+  double* v = nullptr;
+  int64_t* box = nullptr;
+  int64_t* tri = nullptr;
+  int64_t* vis = nullptr;
+  uint8_t* known = nullptr;               // set to 1 for every traced ray
+  unsigned long long* sums = nullptr;     // [0] += boxes, [1] += tris
+};
+
+struct BvhDev {
+  int device = 0;
+  DNode* nodes = nullptr;
+  DTri* tris = nullptr;
+  int32_t* depth = nullptr;
+  int32_t* tri_ids = nullptr;
+  int64_t n_nodes = 0, n_tris = 0;
+  int height = 0;      // longest root-to-leaf edge count (stack bound)
+  int stack = 64;      // template stack size chosen from height
+  std::vector<int32_t> parent_host;
+  std::map<int, int32_t*> anc;  // go-up level -> device LUT
+  ~BvhDev();
+  int ancestor_lut(int level, const int32_t** out);
+};
+
+struct TableDev {
+  int device = 0;
+  int precision = 6, go_up = 0;
+  bool closest = true;
+  int64_t max_entries = 1 << 26;
+  // hash index: key -> entry id
+  unsigned long long* idx_keys = nullptr;
+  int32_t* idx_vals = nullptr;
+  int64_t idx_cap = 0;
+  // entries (creation order), node lists in the arena
+  unsigned long long* e_key = nullptr;
+  int64_t* e_off = nullptr;
+  int32_t* e_len = nullptr;
+  int64_t e_cap = 0;
+  int32_t* arena = nullptr;
+  int64_t arena_cap = 0;
+  // device meta: [0] entries, [1] stored, [2] arena_used
+  long long* meta = nullptr;
+  // host mirrors (exact after every call returns)
+  int64_t n_entries = 0, stored = 0, arena_used = 0;
+  Workspace ws;
+  ~TableDev();
+  int reserve(int64_t extra_rays, cudaStream_t st);  // capacity for a wave of extra_rays
+};
+
+// ---- launchers (return HRPP status) ----
+int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys, int* err,
+                cudaStream_t st);
+int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err,
+                       cudaStream_t st);
+int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
+                 const double* tmin, const double* tmax, int32_t start, int64_t n,
+                 const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
+                 const int* err, cudaStream_t st);
+
+// Group a batch of keys: stable sort (key, ray) and find key segments.
+struct Segments {
+  unsigned long long* skeys = nullptr;
+  int32_t* sidx = nullptr;
+  int32_t* seg_start = nullptr;  // nsegs + 1 entries (device count)
+  int* nsegs = nullptr;          // device scalar
+};
+int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
+                 cudaStream_t st);
+
+struct Consult {
+  bool live = false;
+  const float* O = nullptr;
+  const float* D = nullptr;
+  const double* tmin = nullptr;
+  const double* tmax = nullptr;
+  int64_t n = 0;
+  // per-ray baseline (limit) results
+  const uint8_t* base_found = nullptr;
+  const double* base_t = nullptr;
+  const int32_t* base_leaf = nullptr;
+  const int64_t* base_box = nullptr;
+  // live outputs
+  uint8_t* o_found = nullptr;
+  double* o_t = nullptr;
+  int32_t* o_slot = nullptr;
+  int32_t* o_leaf = nullptr;
+  // limit log
+  int8_t* log_cls = nullptr;
+  int64_t* log_eval_box = nullptr;
+  double* log_pred_t = nullptr;
+  int64_t* log_pred_slot = nullptr;
+};
+
+// Runs the ray-ordered per-key consult of one wave and commits the table.
+// stats_dev: unsigned long long[16] device (RayKindStats order).
+int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* keys,
+                unsigned long long* stats_dev, int* err, cudaStream_t st);
+int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_t n,
+                 uint8_t* inserted, int* err, cudaStream_t st);
+int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
+                 int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st);
+int table_export(TableDev& t, uint64_t* keys_h, int64_t* offs_h, int32_t* nodes_h);
+int table_max_len(TableDev& t, int64_t* out);
+int table_lookup1(TableDev& t, uint64_t key, int32_t* nodes_h, int64_t cap, int64_t* len);
+int predict_batch(const BvhDev& b, TableDev& t, const uint64_t* keys, const float* O,
+                  const float* D, const double* tmin, const double* tmax, int64_t n,
+                  int8_t* cls, double* tt, int32_t* slot, int32_t* leaf, double* u, double* v,
+                  int64_t* box, int64_t* tri, int64_t* vis, int64_t* est, cudaStream_t st);
+
+extern int g_live_rounds;
+
+inline int grid_for(int64_t n, int block, int max_blocks) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+int num_sms();
+
+}  // namespace hrpp

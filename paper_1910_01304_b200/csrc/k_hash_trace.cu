@@ -1,0 +1,188 @@
+// k_hash_trace.cu -- ray hash kernel and full-traversal batch kernel.
+#include "hrpp_internal.h"
+
+namespace hrpp {
+
+// ---------------------------------------------------------------------------
+// Ray hash (hrpp/rayhash.py:99-122).  HBM-bound: 24 B in + 8 B out per ray.
+// Each thread hashes 4 consecutive rays: 3 x 16-B streaming loads each of O
+// and D (48 B = 4 rays x 3 floats), two 16-B key stores.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t lane_hash(uint32_t bits, int p) {
+  uint32_t sign = bits >> 31;
+  uint32_t exp_top = ((bits >> 23) & 0xFFu) >> (8 - p);
+  uint32_t man_top = (bits & 0x7FFFFFu) >> (23 - p);
+  return (sign << (2 * p)) | (exp_top << p) | man_top;
+}
+
+__device__ __forceinline__ bool nonfinite(uint32_t b) { return ((b >> 23) & 0xFFu) == 0xFFu; }
+
+// LANE_PAIRS ((0,2),(1,1),(2,0)) at shifts 0/16/32 (hrpp/rayhash.py:37-39)
+__device__ __forceinline__ uint64_t ray_key(uint32_t ox, uint32_t oy, uint32_t oz, uint32_t dx,
+                                            uint32_t dy, uint32_t dz, int p) {
+  return (uint64_t)(lane_hash(ox, p) ^ lane_hash(dz, p)) |
+         ((uint64_t)(lane_hash(oy, p) ^ lane_hash(dy, p)) << 16) |
+         ((uint64_t)(lane_hash(oz, p) ^ lane_hash(dx, p)) << 32);
+}
+
+__global__ void __launch_bounds__(256) k_hash(const float* __restrict__ O,
+                                              const float* __restrict__ D, int64_t n, int p,
+                                              uint64_t* __restrict__ keys, int* err) {
+  const int64_t nq = (n + 3) / 4;
+  const bool vec = ((reinterpret_cast<uintptr_t>(O) | reinterpret_cast<uintptr_t>(D) |
+                     reinterpret_cast<uintptr_t>(keys)) & 15) == 0;
+  bool bad = false;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = 4 * q;
+    if (vec && i0 + 4 <= n) {
+      const float4* o4 = reinterpret_cast<const float4*>(O + 3 * i0);
+      const float4* d4 = reinterpret_cast<const float4*>(D + 3 * i0);
+      float4 oa = __ldcs(o4), ob = __ldcs(o4 + 1), oc = __ldcs(o4 + 2);
+      float4 da = __ldcs(d4), db = __ldcs(d4 + 1), dc = __ldcs(d4 + 2);
+      uint32_t o[12] = {__float_as_uint(oa.x), __float_as_uint(oa.y), __float_as_uint(oa.z),
+                        __float_as_uint(oa.w), __float_as_uint(ob.x), __float_as_uint(ob.y),
+                        __float_as_uint(ob.z), __float_as_uint(ob.w), __float_as_uint(oc.x),
+                        __float_as_uint(oc.y), __float_as_uint(oc.z), __float_as_uint(oc.w)};
+      uint32_t d[12] = {__float_as_uint(da.x), __float_as_uint(da.y), __float_as_uint(da.z),
+                        __float_as_uint(da.w), __float_as_uint(db.x), __float_as_uint(db.y),
+                        __float_as_uint(db.z), __float_as_uint(db.w), __float_as_uint(dc.x),
+                        __float_as_uint(dc.y), __float_as_uint(dc.z), __float_as_uint(dc.w)};
+#pragma unroll
+      for (int k = 0; k < 12; k++) bad |= nonfinite(o[k]) | nonfinite(d[k]);
+      ulonglong2 k01, k23;
+      k01.x = ray_key(o[0], o[1], o[2], d[0], d[1], d[2], p);
+      k01.y = ray_key(o[3], o[4], o[5], d[3], d[4], d[5], p);
+      k23.x = ray_key(o[6], o[7], o[8], d[6], d[7], d[8], p);
+      k23.y = ray_key(o[9], o[10], o[11], d[9], d[10], d[11], p);
+      ulonglong2* kp = reinterpret_cast<ulonglong2*>(keys + i0);
+      __stcs(kp, k01);
+      __stcs(kp + 1, k23);
+    } else {
+      const int64_t e = i0 + 4 < n ? i0 + 4 : n;
+      for (int64_t i = i0; i < e; i++) {
+        uint32_t o0 = __float_as_uint(O[3 * i]), o1 = __float_as_uint(O[3 * i + 1]),
+                 o2 = __float_as_uint(O[3 * i + 2]);
+        uint32_t d0 = __float_as_uint(D[3 * i]), d1 = __float_as_uint(D[3 * i + 1]),
+                 d2 = __float_as_uint(D[3 * i + 2]);
+        bad |= nonfinite(o0) | nonfinite(o1) | nonfinite(o2) | nonfinite(d0) | nonfinite(d1) |
+               nonfinite(d2);
+        keys[i] = ray_key(o0, o1, o2, d0, d1, d2, p);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
+}
+
+int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys, int* err,
+                cudaStream_t st) {
+  if (n <= 0) return 0;
+  int64_t nq = (n + 3) / 4;
+  int grid = grid_for(nq, 256, num_sms() * 8);
+  k_hash<<<grid, 256, 0, st>>>(O, D, n, p, keys, err);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+// hrpp/rayhash.py:67-78 map_float_to_hash over a float32 array
+__global__ void k_hash_floats(const float* __restrict__ f, int64_t n, int p,
+                              uint32_t* __restrict__ out, int* err) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = __float_as_uint(f[i]);
+    bad |= nonfinite(b);
+    out[i] = lane_hash(b, p);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
+}
+
+int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err,
+                       cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_hash_floats<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(f, n, p, out, err);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Full traversal batch (hrpp/kernels.py:209-248): one ray per thread, f64,
+// per-thread stack in local memory sized from the tree height.  Optional
+// indirection (ray_idx / count_dev) traces a compacted queue of rays.
+// ---------------------------------------------------------------------------
+
+struct TraceArgs {
+  const DNode* nodes;
+  const DTri* tris;
+  const float* O;
+  const float* D;
+  const double* tmin;
+  const double* tmax;
+  int32_t start;
+  int64_t n;
+  const int32_t* ray_idx;
+  const int* count_dev;
+  const int* err;
+  TraceOut out;
+};
+
+template <bool CLOSEST, int STACK>
+__global__ void __launch_bounds__(128) k_trace(TraceArgs a) {
+  if (a.err && *a.err) return;
+  const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.n;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long sb = 0, stt = 0;
+  if (q < count) {
+    const int64_t i = a.ray_idx ? (int64_t)a.ray_idx[q] : q;
+    Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
+    Hit h = trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, a.start);
+    const TraceOut& o = a.out;
+    if (o.found) o.found[i] = h.found;
+    if (o.t) o.t[i] = h.t;
+    if (o.slot) o.slot[i] = h.slot;
+    if (o.leaf) o.leaf[i] = h.leaf;
+    if (CLOSEST && o.u) o.u[i] = h.u;
+    if (CLOSEST && o.v) o.v[i] = h.v;
+    if (o.box) o.box[i] = h.boxes;
+    if (o.tri) o.tri[i] = h.tris;
+    if (o.vis) o.vis[i] = h.boxes;  // visited == box_tests (kernels.py:115-116)
+    if (o.known) o.known[i] = 1;
+    sb = h.boxes;
+    stt = h.tris;
+  }
+  if (a.out.sums) {
+    sb = warp_sum(sb);
+    stt = warp_sum(stt);
+    if ((threadIdx.x & 31) == 0 && (sb | stt)) {
+      atomicAdd(a.out.sums, sb);
+      atomicAdd(a.out.sums + 1, stt);
+    }
+  }
+}
+
+template <bool CLOSEST>
+static void dispatch_trace(int stack, int grid, cudaStream_t st, const TraceArgs& a) {
+  switch (stack) {
+    case 32: k_trace<CLOSEST, 32><<<grid, 128, 0, st>>>(a); break;
+    case 64: k_trace<CLOSEST, 64><<<grid, 128, 0, st>>>(a); break;
+    case 128: k_trace<CLOSEST, 128><<<grid, 128, 0, st>>>(a); break;
+    case 256: k_trace<CLOSEST, 256><<<grid, 128, 0, st>>>(a); break;
+    default: k_trace<CLOSEST, 512><<<grid, 128, 0, st>>>(a); break;
+  }
+}
+
+int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
+                 const double* tmin, const double* tmax, int32_t start, int64_t n,
+                 const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
+                 const int* err, cudaStream_t st) {
+  if (n <= 0) return 0;
+  TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
+  int grid = (int)((n + 127) / 128);
+  if (closest) dispatch_trace<true>(b.stack, grid, st, a);
+  else dispatch_trace<false>(b.stack, grid, st, a);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+}  // namespace hrpp

@@ -1,0 +1,572 @@
+// k_table.cu -- predictor table in HBM (hrpp/predictor.py:117-211).
+//
+// Index: open-addressed (linear probing) buckets {u64 key, i32 entry id},
+// load factor <= 0.5, inserted with atomicCAS.  Entries: SoA {key, arena
+// offset, length} in creation order.  Node lists live contiguously in an
+// int32 arena; an entry that grows during a wave is relocated to the arena
+// tail (old list + appended nodes), so every list stays contiguous for the
+// consult kernel's broadcast reads.  The arena is compacted when garbage
+// would overflow it.
+#include <cub/cub.cuh>
+
+#include "hrpp_internal.h"
+
+namespace hrpp {
+
+// ---------------------------------------------------------------------------
+// grouping: stable (key, ray) sort + key segments
+// ---------------------------------------------------------------------------
+
+__global__ void k_iota(int32_t* v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+__global__ void k_head_flags(const unsigned long long* __restrict__ sk, int64_t n,
+                             uint8_t* __restrict__ flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0) || (sk[i] != sk[i - 1]);
+}
+
+__global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n) {
+  seg_start[*nsegs] = (int32_t)n;
+}
+
+int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
+                 cudaStream_t st) {
+  int32_t* iota;
+  uint8_t* flags;
+  int rc;
+  if ((rc = ws.get("g_skeys", n, &seg->skeys))) return rc;
+  if ((rc = ws.get("g_iota", n, &iota))) return rc;
+  if ((rc = ws.get("g_sidx", n, &seg->sidx))) return rc;
+  if ((rc = ws.get("g_flags", n, &flags))) return rc;
+  if ((rc = ws.get("g_segstart", n + 1, &seg->seg_start))) return rc;
+  if ((rc = ws.get("g_nsegs", 1, &seg->nsegs))) return rc;
+  int grid = grid_for(n, 256, num_sms() * 8);
+  k_iota<<<grid, 256, 0, st>>>(iota, n);
+  HRPP_LAUNCHED();
+  const unsigned long long* kin = reinterpret_cast<const unsigned long long*>(keys);
+  size_t b_sort = 0, b_sel = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b_sort, kin, seg->skeys, iota, seg->sidx, (int)n,
+                                  0, 48, st);
+  cub::CountingInputIterator<int32_t> cnt(0);
+  cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
+                             st);
+  void* tmp;
+  if ((rc = ws.get_raw("g_cubtmp", b_sort > b_sel ? b_sort : b_sel, &tmp))) return rc;
+  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b_sort, kin, seg->skeys, iota, seg->sidx, (int)n,
+                                          0, 48, st));
+  k_head_flags<<<grid, 256, 0, st>>>(seg->skeys, n, flags);
+  HRPP_LAUNCHED();
+  HRPP_CK(cub::DeviceSelect::Flagged(tmp, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
+                                     st));
+  k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// index maintenance
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void index_insert(unsigned long long* keys, int32_t* vals,
+                                             uint64_t mask, unsigned long long key,
+                                             int32_t id) {
+  uint64_t h = mix64(key) & mask;
+  for (;;) {
+    unsigned long long prev = atomicCAS(keys + h, kEmptyKey, key);
+    if (prev == kEmptyKey || prev == key) {
+      vals[h] = id;
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void k_rehash(const unsigned long long* __restrict__ e_key, int64_t n_entries,
+                         unsigned long long* keys, int32_t* vals, uint64_t mask) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
+       e += (int64_t)gridDim.x * blockDim.x)
+    index_insert(keys, vals, mask, e_key[e], (int32_t)e);
+}
+
+__global__ void k_len_to_i64(const int32_t* __restrict__ len, int64_t n, long long* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = len[i];
+}
+
+__global__ void k_compact(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                          int64_t* e_off, const int32_t* __restrict__ e_len,
+                          const long long* __restrict__ new_off, int64_t n_entries) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = e_off[e], no = new_off[e];
+    for (int32_t j = 0; j < e_len[e]; j++) dst[no + j] = src[o + j];
+    e_off[e] = no;
+  }
+}
+
+static int64_t next_pow2(int64_t x) {
+  int64_t p = 1024;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+template <typename T>
+static int grow(T** p, int64_t old_count, int64_t new_count, cudaStream_t st) {
+  T* np = nullptr;
+  HRPP_CK(cudaMalloc(&np, sizeof(T) * new_count));
+  if (*p && old_count) HRPP_CK(cudaMemcpyAsync(np, *p, sizeof(T) * old_count,
+                                               cudaMemcpyDeviceToDevice, st));
+  if (*p) {
+    HRPP_CK(cudaStreamSynchronize(st));
+    HRPP_CK(cudaFree(*p));
+  }
+  *p = np;
+  return 0;
+}
+
+int TableDev::reserve(int64_t extra, cudaStream_t st) {
+  int rc;
+  if (!meta) {
+    HRPP_CK(cudaMalloc(&meta, sizeof(long long) * 4));
+    HRPP_CK(cudaMemsetAsync(meta, 0, sizeof(long long) * 4, st));
+  }
+  int64_t need_e = n_entries + extra + 16;
+  if (e_cap < need_e) {
+    int64_t nc = need_e > 2 * e_cap ? need_e : 2 * e_cap;
+    if ((rc = grow(&e_key, n_entries, nc, st))) return rc;
+    if ((rc = grow(&e_off, n_entries, nc, st))) return rc;
+    if ((rc = grow(&e_len, n_entries, nc, st))) return rc;
+    e_cap = nc;
+  }
+  int64_t need_idx = next_pow2(2 * need_e);
+  if (idx_cap < need_idx) {
+    if (idx_keys) {
+      HRPP_CK(cudaStreamSynchronize(st));
+      HRPP_CK(cudaFree(idx_keys));
+      HRPP_CK(cudaFree(idx_vals));
+    }
+    HRPP_CK(cudaMalloc(&idx_keys, sizeof(unsigned long long) * need_idx));
+    HRPP_CK(cudaMalloc(&idx_vals, sizeof(int32_t) * need_idx));
+    HRPP_CK(cudaMemsetAsync(idx_keys, 0xFF, sizeof(unsigned long long) * need_idx, st));
+    idx_cap = need_idx;
+    if (n_entries) {
+      k_rehash<<<grid_for(n_entries, 256, num_sms() * 8), 256, 0, st>>>(
+          e_key, n_entries, idx_keys, idx_vals, (uint64_t)idx_cap - 1);
+      HRPP_LAUNCHED();
+    }
+  }
+  int64_t need_arena = arena_used + stored + extra + 16;
+  if (arena_cap < need_arena) {
+    // compact live lists into a fresh arena sized with headroom
+    int64_t nc = 2 * (stored + extra) + 1024;
+    if (nc < 2 * arena_cap && arena_used <= 2 * stored) nc = 2 * arena_cap;
+    int32_t* na = nullptr;
+    HRPP_CK(cudaMalloc(&na, sizeof(int32_t) * nc));
+    if (n_entries) {
+      long long *len64, *off64;
+      if ((rc = ws.get("c_len64", n_entries, &len64))) return rc;
+      if ((rc = ws.get("c_off64", n_entries, &off64))) return rc;
+      int grid = grid_for(n_entries, 256, num_sms() * 8);
+      k_len_to_i64<<<grid, 256, 0, st>>>(e_len, n_entries, len64);
+      HRPP_LAUNCHED();
+      size_t b = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, b, len64, off64, (int)n_entries, st);
+      void* tmp;
+      if ((rc = ws.get_raw("c_tmp", b, &tmp))) return rc;
+      HRPP_CK(cub::DeviceScan::ExclusiveSum(tmp, b, len64, off64, (int)n_entries, st));
+      k_compact<<<grid, 256, 0, st>>>(arena, na, e_off, e_len, off64, n_entries);
+      HRPP_LAUNCHED();
+    }
+    if (arena) {
+      HRPP_CK(cudaStreamSynchronize(st));
+      HRPP_CK(cudaFree(arena));
+    }
+    arena = na;
+    arena_cap = nc;
+    arena_used = stored;
+    long long used = stored;
+    HRPP_CK(cudaMemcpyAsync(meta + 2, &used, sizeof(long long), cudaMemcpyHostToDevice, st));
+    HRPP_CK(cudaStreamSynchronize(st));
+  }
+  return 0;
+}
+
+TableDev::~TableDev() {
+  cudaFree(idx_keys);
+  cudaFree(idx_vals);
+  cudaFree(e_key);
+  cudaFree(e_off);
+  cudaFree(e_len);
+  cudaFree(arena);
+  cudaFree(meta);
+}
+
+// ---------------------------------------------------------------------------
+// commit the per-segment appends of one wave (or one record batch)
+// ---------------------------------------------------------------------------
+
+struct Trip {
+  long long n_new, reloc, app;
+};
+struct TripSum {
+  __host__ __device__ Trip operator()(const Trip& a, const Trip& b) const {
+    return Trip{a.n_new + b.n_new, a.reloc + b.reloc, a.app + b.app};
+  }
+};
+
+__global__ void k_commit_prepare(const int* nsegs, int64_t n, const int32_t* __restrict__ seg_eid,
+                                 const int32_t* __restrict__ seg_napp,
+                                 const int32_t* __restrict__ e_len, Trip* vals, const int* err) {
+  const int ns = *nsegs;
+  const bool dead = *err != 0;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    Trip v{0, 0, 0};
+    if (s < ns && !dead) {
+      int32_t napp = seg_napp[s], eid = seg_eid[s];
+      if (napp > 0) {
+        v.n_new = eid < 0;
+        v.reloc = (eid >= 0 ? e_len[eid] : 0) + napp;
+        v.app = napp;
+      }
+    }
+    vals[s] = v;
+  }
+}
+
+__global__ void k_commit_check(const Trip* vals, const Trip* scan, int64_t n,
+                               const long long* meta, long long max_entries, int* err,
+                               long long* totals) {
+  Trip t = TripSum()(vals[n - 1], scan[n - 1]);
+  totals[0] = t.n_new;
+  totals[1] = t.reloc;
+  totals[2] = t.app;
+  if (*err == 0 && meta[0] + t.n_new > max_entries) *err = 2;  // CapacityExceeded
+}
+
+__global__ void k_commit_apply(const int* nsegs, const int32_t* __restrict__ seg_start,
+                               const unsigned long long* __restrict__ skeys,
+                               const int32_t* __restrict__ seg_eid,
+                               const int32_t* __restrict__ seg_napp,
+                               const int32_t* __restrict__ app, const Trip* __restrict__ scan,
+                               const long long* meta, unsigned long long* e_key,
+                               int64_t* e_off, int32_t* e_len, int32_t* arena,
+                               unsigned long long* idx_keys, int32_t* idx_vals, uint64_t mask,
+                               const int* err) {
+  if (*err) return;
+  const int ns = *nsegs;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+    int32_t napp = seg_napp[s];
+    if (napp <= 0) continue;
+    int32_t eid = seg_eid[s];
+    int32_t old_len = 0;
+    int64_t old_off = 0;
+    if (eid >= 0) {
+      old_len = e_len[eid];
+      old_off = e_off[eid];
+    } else {
+      eid = (int32_t)(meta[0] + scan[s].n_new);
+      unsigned long long key = skeys[seg_start[s]];
+      e_key[eid] = key;
+      index_insert(idx_keys, idx_vals, mask, key, eid);
+    }
+    int64_t no = meta[2] + scan[s].reloc;
+    for (int32_t j = 0; j < old_len; j++) arena[no + j] = arena[old_off + j];
+    const int32_t* a = app + seg_start[s];
+    for (int32_t j = 0; j < napp; j++) arena[no + old_len + j] = a[j];
+    e_off[eid] = no;
+    e_len[eid] = old_len + napp;
+  }
+}
+
+__global__ void k_commit_finish(long long* meta, const long long* totals, const int* err) {
+  if (*err) return;
+  meta[0] += totals[0];
+  meta[1] += totals[2];
+  meta[2] += totals[1];
+}
+
+int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
+                 int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st) {
+  Trip *vals, *scan;
+  long long* totals;
+  int rc;
+  if ((rc = t.ws.get("m_vals", n, &vals))) return rc;
+  if ((rc = t.ws.get("m_scan", n, &scan))) return rc;
+  if ((rc = t.ws.get("m_tot", 4, &totals))) return rc;
+  int grid = grid_for(n, 256, num_sms() * 8);
+  k_commit_prepare<<<grid, 256, 0, st>>>(seg.nsegs, n, seg_eid, seg_napp, t.e_len, vals, err);
+  HRPP_LAUNCHED();
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, b, vals, scan, TripSum(), Trip{0, 0, 0}, (int)n, st);
+  void* tmp;
+  if ((rc = t.ws.get_raw("m_tmp", b, &tmp))) return rc;
+  HRPP_CK(cub::DeviceScan::ExclusiveScan(tmp, b, vals, scan, TripSum(), Trip{0, 0, 0}, (int)n,
+                                         st));
+  k_commit_check<<<1, 1, 0, st>>>(vals, scan, n, t.meta, (long long)t.max_entries, err, totals);
+  HRPP_LAUNCHED();
+  k_commit_apply<<<grid, 256, 0, st>>>(seg.nsegs, seg.seg_start, seg.skeys, seg_eid, seg_napp,
+                                       app, scan, t.meta, t.e_key, t.e_off, t.e_len, t.arena,
+                                       t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, err);
+  HRPP_LAUNCHED();
+  k_commit_finish<<<1, 1, 0, st>>>(t.meta, totals, err);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// record (predictor.py:147-160), batched with sequential semantics
+// ---------------------------------------------------------------------------
+
+__global__ void k_record_seg(const int* nsegs, const int32_t* __restrict__ seg_start,
+                             const unsigned long long* __restrict__ skeys,
+                             const int32_t* __restrict__ sidx, const int32_t* __restrict__ nodes,
+                             const unsigned long long* __restrict__ idx_keys,
+                             const int32_t* __restrict__ idx_vals, uint64_t mask,
+                             const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_len,
+                             const int32_t* __restrict__ arena, int32_t* app, int32_t* seg_eid,
+                             int32_t* seg_napp, uint8_t* inserted) {
+  const int ns = *nsegs;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+    int32_t beg = seg_start[s], end = seg_start[s + 1];
+    int32_t eid = index_lookup(idx_keys, idx_vals, mask, skeys[beg]);
+    int64_t off = eid >= 0 ? e_off[eid] : 0;
+    int32_t len = eid >= 0 ? e_len[eid] : 0;
+    int32_t* ap = app + beg;
+    int32_t napp = 0;
+    for (int32_t j = beg; j < end; j++) {
+      int32_t idx = sidx[j];
+      int32_t node = nodes[idx];
+      bool dup = false;
+      for (int32_t k = 0; k < len && !dup; k++) dup = arena[off + k] == node;
+      for (int32_t k = 0; k < napp && !dup; k++) dup = ap[k] == node;
+      if (!dup) ap[napp++] = node;
+      if (inserted) inserted[idx] = !dup;
+    }
+    seg_eid[s] = eid;
+    seg_napp[s] = napp;
+  }
+}
+
+int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_t n,
+                 uint8_t* inserted, int* err, cudaStream_t st) {
+  int rc;
+  if ((rc = t.reserve(n, st))) return rc;
+  Segments seg;
+  if ((rc = group_by_key(t.ws, keys, n, &seg, st))) return rc;
+  int32_t *app, *seg_eid, *seg_napp;
+  if ((rc = t.ws.get("r_app", n, &app))) return rc;
+  if ((rc = t.ws.get("r_eid", n, &seg_eid))) return rc;
+  if ((rc = t.ws.get("r_napp", n, &seg_napp))) return rc;
+  k_record_seg<<<grid_for(n, 128, num_sms() * 16), 128, 0, st>>>(
+      seg.nsegs, seg.seg_start, seg.skeys, seg.sidx, nodes, t.idx_keys, t.idx_vals,
+      (uint64_t)t.idx_cap - 1, t.e_off, t.e_len, t.arena, app, seg_eid, seg_napp, inserted);
+  HRPP_LAUNCHED();
+  return table_commit(t, seg, n, seg_eid, seg_napp, app, err, st);
+}
+
+// ---------------------------------------------------------------------------
+// export (dump_lines order), lookup, max length
+// ---------------------------------------------------------------------------
+
+__global__ void k_export_len(const int32_t* __restrict__ ids, const int32_t* __restrict__ e_len,
+                             int64_t n, long long* lens) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lens[i] = e_len[ids[i]];
+}
+
+__global__ void k_export_nodes(const int32_t* __restrict__ ids, const int64_t* __restrict__ e_off,
+                               const int32_t* __restrict__ e_len, const int32_t* __restrict__ arena,
+                               const long long* __restrict__ offs, int64_t n, int32_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t e = ids[i];
+    int64_t o = e_off[e];
+    for (int32_t j = 0; j < e_len[e]; j++) out[offs[i] + j] = arena[o + j];
+  }
+}
+
+int table_export(TableDev& t, uint64_t* keys_h, int64_t* offs_h, int32_t* nodes_h) {
+  const int64_t n = t.n_entries;
+  offs_h[0] = 0;
+  if (n == 0) return 0;
+  cudaStream_t st = 0;
+  int rc;
+  unsigned long long* sk;
+  int32_t *iota, *ids, *nodes;
+  long long *lens, *offs;
+  if ((rc = t.ws.get("x_sk", n, &sk))) return rc;
+  if ((rc = t.ws.get("x_iota", n, &iota))) return rc;
+  if ((rc = t.ws.get("x_ids", n, &ids))) return rc;
+  if ((rc = t.ws.get("x_len", n + 1, &lens))) return rc;
+  if ((rc = t.ws.get("x_off", n + 1, &offs))) return rc;
+  if ((rc = t.ws.get("x_nodes", t.stored + 1, &nodes))) return rc;
+  int grid = grid_for(n, 256, num_sms() * 8);
+  k_iota<<<grid, 256, 0, st>>>(iota, n);
+  HRPP_LAUNCHED();
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b1, t.e_key, sk, iota, ids, (int)n, 0, 48, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, b2, lens, offs, (int)n + 1, st);
+  void* tmp;
+  if ((rc = t.ws.get_raw("x_tmp", b1 > b2 ? b1 : b2, &tmp))) return rc;
+  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b1, t.e_key, sk, iota, ids, (int)n, 0, 48, st));
+  HRPP_CK(cudaMemsetAsync(lens + n, 0, sizeof(long long), st));
+  k_export_len<<<grid, 256, 0, st>>>(ids, t.e_len, n, lens);
+  HRPP_LAUNCHED();
+  HRPP_CK(cub::DeviceScan::ExclusiveSum(tmp, b2, lens, offs, (int)n + 1, st));
+  k_export_nodes<<<grid, 256, 0, st>>>(ids, t.e_off, t.e_len, t.arena, offs, n, nodes);
+  HRPP_LAUNCHED();
+  HRPP_CK(cudaMemcpyAsync(keys_h, sk, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, st));
+  HRPP_CK(cudaMemcpyAsync(offs_h, offs, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (t.stored)
+    HRPP_CK(cudaMemcpyAsync(nodes_h, nodes, sizeof(int32_t) * t.stored, cudaMemcpyDeviceToHost,
+                            st));
+  HRPP_CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+__global__ void k_lookup1(const unsigned long long* __restrict__ idx_keys,
+                          const int32_t* __restrict__ idx_vals, uint64_t mask, uint64_t key,
+                          const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_len,
+                          long long* out) {
+  int32_t e = idx_keys ? index_lookup(idx_keys, idx_vals, mask, key) : -1;
+  out[0] = e >= 0 ? e_off[e] : 0;
+  out[1] = e >= 0 ? e_len[e] : 0;
+}
+
+int table_lookup1(TableDev& t, uint64_t key, int32_t* nodes_h, int64_t cap, int64_t* len) {
+  *len = 0;
+  if (t.n_entries == 0) return 0;
+  long long* out;
+  int rc;
+  if ((rc = t.ws.get("l_out", 2, &out))) return rc;
+  k_lookup1<<<1, 1>>>(t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, key, t.e_off, t.e_len, out);
+  HRPP_LAUNCHED();
+  long long h[2];
+  HRPP_CK(cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost));
+  *len = h[1];
+  int64_t m = h[1] < cap ? h[1] : cap;
+  if (m > 0 && nodes_h)
+    HRPP_CK(cudaMemcpy(nodes_h, t.arena + h[0], sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int table_max_len(TableDev& t, int64_t* out) {
+  *out = 0;
+  if (t.n_entries == 0) return 0;
+  int32_t* r;
+  int rc;
+  if ((rc = t.ws.get("mx_out", 1, &r))) return rc;
+  size_t b = 0;
+  cub::DeviceReduce::Max(nullptr, b, t.e_len, r, (int)t.n_entries);
+  void* tmp;
+  if ((rc = t.ws.get_raw("mx_tmp", b, &tmp))) return rc;
+  HRPP_CK(cub::DeviceReduce::Max(tmp, b, t.e_len, r, (int)t.n_entries));
+  int32_t h = 0;
+  HRPP_CK(cudaMemcpy(&h, r, sizeof(h), cudaMemcpyDeviceToHost));
+  *out = h;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// predict (hrpp/predictor.py:167-192) against a frozen table
+// ---------------------------------------------------------------------------
+
+struct PredictArgs {
+  const DNode* nodes;
+  const DTri* tris;
+  const int32_t* depth;
+  const unsigned long long* idx_keys;
+  const int32_t* idx_vals;
+  uint64_t mask;
+  const int64_t* e_off;
+  const int32_t* e_len;
+  const int32_t* arena;
+  const uint64_t* keys;
+  const float* O;
+  const float* D;
+  const double* tmin;
+  const double* tmax;
+  int64_t n;
+  int8_t* cls;
+  double* t;
+  int32_t* slot;
+  int32_t* leaf;
+  double* u;
+  double* v;
+  int64_t* box;
+  int64_t* tri;
+  int64_t* vis;
+  int64_t* est;
+};
+
+template <bool CLOSEST, int STACK>
+__global__ void __launch_bounds__(128) k_predict(PredictArgs a) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  int32_t e = a.idx_keys ? index_lookup(a.idx_keys, a.idx_vals, a.mask, a.keys[i]) : -1;
+  Hit acc = empty_entry_result(CLOSEST);
+  int8_t c = 2;
+  if (e >= 0) {
+    Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
+    const int32_t* nl = a.arena + a.e_off[e];
+    int32_t L = a.e_len[e];
+    for (int32_t j = 0; j < L; j++) {
+      if (!CLOSEST && acc.found) break;  // eval_entry_any stops at the first hit
+      fold_entry<CLOSEST>(acc, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, nl[j]));
+    }
+    c = acc.found ? 0 : 1;
+  } else {
+    acc.t = __longlong_as_double(0x7ff0000000000000LL);
+  }
+  a.cls[i] = c;
+  if (a.t) a.t[i] = acc.t;
+  if (a.slot) a.slot[i] = acc.slot;
+  if (a.leaf) a.leaf[i] = acc.leaf;
+  if (a.u) a.u[i] = acc.u;
+  if (a.v) a.v[i] = acc.v;
+  if (a.box) a.box[i] = acc.boxes;
+  if (a.tri) a.tri[i] = acc.tris;
+  if (a.vis) a.vis[i] = acc.boxes;
+  if (a.est) {
+    int64_t x = acc.found ? (int64_t)a.depth[acc.leaf] + 1 - acc.boxes : 0;
+    a.est[i] = x > 0 ? x : 0;
+  }
+}
+
+int predict_batch(const BvhDev& b, TableDev& t, const uint64_t* keys, const float* O,
+                  const float* D, const double* tmin, const double* tmax, int64_t n,
+                  int8_t* cls, double* tt, int32_t* slot, int32_t* leaf, double* u, double* v,
+                  int64_t* box, int64_t* tri, int64_t* vis, int64_t* est, cudaStream_t st) {
+  if (n <= 0) return 0;
+  PredictArgs a{b.nodes, b.tris, b.depth, t.n_entries ? t.idx_keys : nullptr, t.idx_vals,
+                (uint64_t)t.idx_cap - 1, t.e_off, t.e_len, t.arena, keys, O, D, tmin, tmax, n,
+                cls, tt, slot, leaf, u, v, box, tri, vis, est};
+  int grid = (int)((n + 127) / 128);
+#define PRED_CASE(S)                                                        \
+  case S:                                                                   \
+    if (t.closest) k_predict<true, S><<<grid, 128, 0, st>>>(a);             \
+    else k_predict<false, S><<<grid, 128, 0, st>>>(a);                      \
+    break;
+  switch (b.stack) {
+    PRED_CASE(32)
+    PRED_CASE(64)
+    PRED_CASE(128)
+    PRED_CASE(256)
+    default:
+      if (t.closest) k_predict<true, 512><<<grid, 128, 0, st>>>(a);
+      else k_predict<false, 512><<<grid, 128, 0, st>>>(a);
+  }
+#undef PRED_CASE
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+}  // namespace hrpp

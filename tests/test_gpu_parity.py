@@ -1,0 +1,426 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and against the pinned C oracle.
+
+Bar (BASELINE.json north_star): keys bit-exact; hit flags, slots/triangle
+ids, leaves and all counters exact; t / u / v bit-exact too (the kernels
+restate the reference's float64 arithmetic without FMA), which is stricter
+than the stated 1e-5 relative tolerance; statistics, outcome logs and table
+dumps exact (deterministic ray-ordered mode).
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+WAVES = ("primary", "shadow", "reflection")
+SETTINGS = ((6, 0), (3, 0), (4, 2), (7, 1))
+
+
+@pytest.fixture(scope="module")
+def hb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1910_01304_b200 as m
+    return m
+
+
+def gbvh(hb, name):
+    g = load_golden(f"bvh_{name}.npz")
+    return hb.Bvh(g["bmin"], g["bmax"], g["left"], g["right"], g["axis"], g["first"], g["count"],
+                  g["parent"], g["depth"], g["tv0"], g["tv1"], g["tv2"], g["tri_ids"],
+                  int(g["max_depth"]))
+
+
+# -- hash ----------------------------------------------------------------------
+
+def test_hash_keys_bit_exact(hb):
+    g = load_golden("hash.npz")
+    for p in range(1, 8):
+        keys = hb.hash_rays(g["O"], g["D"], hb.HashConfig(p))
+        assert keys.dtype == np.uint64
+        assert np.array_equal(keys, g["keys"][p - 1]), p
+
+
+def test_hash_unaligned_and_ragged(hb):
+    g = load_golden("hash.npz")
+    for n in (0, 1, 2, 3, 5, 7, 4093):
+        for off in (0, 1):
+            O = g["O"][off:off + n]
+            D = g["D"][off:off + n]
+            keys = hb.hash_rays(O, D, hb.HashConfig(6))
+            assert np.array_equal(keys, g["keys"][5][off:off + n])
+
+
+def test_hash_known_answers_and_scalars(hb):
+    cfg2 = hb.HashConfig(2)
+    assert hb.map_float_to_hash(1.0, cfg2) == 4
+    assert hb.map_float_to_hash(-1.0, cfg2) == 20
+    for p in range(1, 8):
+        assert hb.map_float_to_hash(0.0, hb.HashConfig(p)) == 0
+    g = load_golden("hash.npz")
+    for p in range(1, 8):
+        got = [hb.map_float_to_hash(float(f), hb.HashConfig(p)) for f in g["special"]]
+        assert got == g["special_hash"][p - 1].tolist()
+    assert hb.hash_ray_components(1, 1, 1, 1, 1, 1, cfg2) == 0
+    for bad in (float("nan"), float("inf"), float("-inf"), 1e300):
+        with pytest.raises(hb.NonFiniteInput):
+            hb.map_float_to_hash(bad, hb.HashConfig(3))
+
+
+def test_hash_rejects_non_finite(hb):
+    O = np.zeros((2, 3), np.float32)
+    D = np.array([[0, 0, 1], [0, np.nan, 1]], np.float32)
+    with pytest.raises(hb.NonFiniteInput):
+        hb.hash_rays(O, D, hb.HashConfig(3))
+
+
+def test_hash_torch_zero_copy(hb):
+    import torch
+    g = load_golden("hash.npz")
+    O = torch.from_numpy(g["O"]).cuda()
+    D = torch.from_numpy(g["D"]).cuda()
+    keys = hb.hash_rays(O, D, hb.HashConfig(5))
+    assert keys.is_cuda
+    assert np.array_equal(keys.cpu().numpy(), g["keys"][4])
+
+
+# -- traversal batch ---------------------------------------------------------------
+
+def test_trace_batch_matches_reference(hb):
+    g = load_golden("trace_soup256.npz")
+    b = gbvh(hb, "soup256")
+    n = g["O"].shape[0]
+    c = hb.intersect_closest_batch(b, g["O"], g["D"], np.zeros(n), np.full(n, np.inf))
+    for k, v in c.items():
+        assert np.array_equal(v, g[f"c_{k}"]), k
+    a = hb.intersect_any_batch(b, g["O"], g["D"], np.zeros(n), g["tmax_any"])
+    for k, v in a.items():
+        assert np.array_equal(v, g[f"a_{k}"]), k
+    c7 = hb.intersect_closest_batch(b, g["O"], g["D"], np.zeros(n), np.full(n, np.inf), start=7)
+    for k, v in c7.items():
+        assert np.array_equal(v, g[f"c7_{k}"]), k
+
+
+def test_trace_axis_aligned_rays(hb):
+    g = load_golden("trace_strip8.npz")
+    b = gbvh(hb, "strip8")
+    n = g["O"].shape[0]
+    c = hb.intersect_closest_batch(b, g["O"], g["D"], np.zeros(n), np.full(n, np.inf))
+    for k, v in c.items():
+        assert np.array_equal(v, g[f"c_{k}"]), k
+    a = hb.intersect_any_batch(b, g["O"], g["D"], np.zeros(n), np.full(n, 100.0))
+    for k, v in a.items():
+        assert np.array_equal(v, g[f"a_{k}"]), k
+
+
+def test_single_ray_api(hb):
+    b = gbvh(hb, "strip8")
+    r = hb.Ray(hb.vec3(0.25, 0.25, -5.0), hb.vec3(0, 0, 1))
+    c = hb.TraversalCounters()
+    h = hb.intersect_closest(b, r, c)
+    assert h is not None and h.triangle_id == 0 and c.box_tests >= 1
+    sub = hb.intersect_from_node(b, h.leaf_node, r, hb.TraversalCounters())
+    assert sub.t == h.t
+    with pytest.raises(ValueError):
+        hb.intersect_any(b, r, hb.TraversalCounters())
+    with pytest.raises(ValueError):
+        hb.intersect_from_node(b, b.node_count, r, hb.TraversalCounters())
+    assert hb.intersect_closest(b, hb.Ray(hb.vec3(50, 50, -5), hb.vec3(0, 0, 1)),
+                                hb.TraversalCounters()) is None
+
+
+def test_trace_vs_oracle_spheres_random(hb, oracle_mod):
+    from oracle.oracle import OracleBvh
+    g = load_golden("bvh_spheres.npz")
+    b = gbvh(hb, "spheres")
+    ob = OracleBvh.from_dict(g)
+    rng = np.random.default_rng(3)
+    n = 200_000
+    O = rng.uniform(-12, 12, (n, 3)).astype(np.float32)
+    O[:, 1] = np.abs(O[:, 1]) + 0.5
+    D = rng.normal(size=(n, 3))
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    D = D.astype(np.float32)
+    D[:1000, 0] = 0.0  # zero components: signed-infinity reciprocal
+    D[1000:2000, 2] = -0.0
+    tmax = rng.uniform(0.5, 30.0, n)
+    for closest in (True, False):
+        got = (hb.intersect_closest_batch if closest else hb.intersect_any_batch)(
+            b, O, D, np.zeros(n), tmax)
+        ref = ob.trace_batch(closest, O, D, np.zeros(n), tmax)
+        for k, v in ref.items():
+            assert np.array_equal(got[k], v), (closest, k)
+
+
+# -- the wave (limit / live / baseline) ----------------------------------------------
+
+@pytest.mark.parametrize("p,g_", SETTINGS)
+@pytest.mark.parametrize("mode", ["limit", "live"])
+def test_wave_sequence_matches_reference(hb, p, g_, mode):
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden(f"wave_{mode}_p{p}_g{g_}.npz")
+    b = gbvh(hb, "spheres")
+    cfg = hb.HashConfig(p)
+    tables = {True: hb.PredictorTable(cfg, g_, hb.RayKind.CLOSEST_HIT),
+              False: hb.PredictorTable(cfg, g_, hb.RayKind.HIT_ANY)}
+    for w in WAVES:
+        closest = w != "shadow"
+        stats = hb.RayKindStats()
+        ll = ({"cls": [], "eval_box": [], "base_box": [], "pred_t": [], "pred_slot": [],
+               "keys": []} if mode == "limit" else None)
+        out = hb._trace_wave(b, tables[closest], None, hb.RenderMode(mode), inp[f"{w}_O"],
+                             inp[f"{w}_D"], inp[f"{w}_tmin"], inp[f"{w}_tmax"], stats,
+                             closest=closest, log_lists=ll)
+        assert np.array_equal(stats.as_array(), ref[f"{w}_stats"]), (w, stats)
+        for k in ("found", "t", "slot", "leaf", "u", "v", "box", "tri", "visited"):
+            if f"{w}_{k}" in ref:
+                assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
+        if ll is not None:
+            for k in ("cls", "eval_box", "base_box", "pred_t", "pred_slot", "keys"):
+                assert np.array_equal(np.array(ll[k]), ref[f"{w}_log_{k}"]), (w, k)
+        assert list(tables[closest].dump_lines()) == list(ref[f"{w}_dump"]), w
+        ts = hb.table_stats(tables[closest])
+        assert [ts.entries, ts.stored_nodes, ts.max_nodes_per_entry,
+                ts.memory.total_bytes] == list(ref[f"{w}_tstats"])
+
+
+def test_baseline_mode(hb):
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden("wave_limit_p6_g0.npz")
+    b = gbvh(hb, "spheres")
+    stats = hb.RayKindStats()
+    out = hb._trace_wave(b, None, None, hb.RenderMode.BASELINE, inp["primary_O"],
+                         inp["primary_D"], inp["primary_tmin"], inp["primary_tmax"], stats,
+                         closest=True, log_lists=None)
+    assert np.array_equal(out["found"], ref["primary_found"])
+    assert np.array_equal(out["t"], ref["primary_t"])
+    assert stats.consulted == 0
+    assert stats.baseline_box_tests == ref["primary_stats"][4]
+
+
+@pytest.mark.parametrize("rounds", [0, 1, 2, 7])
+def test_live_rounds_do_not_change_results(hb, rounds):
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden("wave_live_p3_g0.npz")  # long key segments at p=3
+    b = gbvh(hb, "spheres")
+    hb.set_live_rounds(rounds)
+    try:
+        t = hb.PredictorTable(hb.HashConfig(3), 0, hb.RayKind.CLOSEST_HIT)
+        stats = hb.RayKindStats()
+        out = hb._trace_wave(b, t, None, hb.RenderMode.LIVE, inp["primary_O"], inp["primary_D"],
+                             inp["primary_tmin"], inp["primary_tmax"], stats, closest=True,
+                             log_lists=None)
+        assert np.array_equal(stats.as_array(), ref["primary_stats"])
+        for k in ("found", "t", "slot", "leaf"):
+            assert np.array_equal(out[k], ref[f"primary_{k}"]), k
+        assert list(t.dump_lines()) == list(ref["primary_dump"])
+    finally:
+        hb.set_live_rounds(3)
+
+
+def test_wave_torch_device_arrays(hb):
+    import torch
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden("wave_live_p6_g0.npz")
+    b = gbvh(hb, "spheres")
+    t = hb.PredictorTable(hb.HashConfig(6), 0, hb.RayKind.CLOSEST_HIT)
+    cu = lambda k: torch.from_numpy(inp[k]).cuda()  # noqa: E731
+    out, stats = hb.trace_wave(b, t, "live", cu("primary_O"), cu("primary_D"),
+                               cu("primary_tmin"), cu("primary_tmax"), closest=True)
+    assert out["found"].is_cuda
+    assert np.array_equal(stats, ref["primary_stats"])
+    assert np.array_equal(out["t"].cpu().numpy(), ref["primary_t"])
+
+
+def test_wave_rejects_non_finite_and_kind_mismatch(hb):
+    b = gbvh(hb, "strip8")
+    t = hb.PredictorTable(hb.HashConfig(6), 0, hb.RayKind.CLOSEST_HIT)
+    O = np.zeros((3, 3), np.float32)
+    D = np.array([[0, 0, 1], [0, 0, 1], [np.inf, 0, 1]], np.float32)
+    stats = hb.RayKindStats()
+    with pytest.raises(hb.NonFiniteInput):
+        hb._trace_wave(b, t, None, hb.RenderMode.LIMIT, O, D, np.zeros(3), np.full(3, np.inf),
+                       stats, closest=True, log_lists=None)
+    assert stats.rays == 3 and stats.consulted == 0 and t.entry_count == 0
+    with pytest.raises(ValueError):
+        hb.trace_wave(b, t, "limit", O[:2], D[:2], np.zeros(2), np.ones(2), closest=False)
+
+
+def test_wave_capacity_exceeded(hb):
+    inp = load_golden("wave_inputs.npz")
+    b = gbvh(hb, "spheres")
+    t = hb.PredictorTable(hb.HashConfig(6), 0, hb.RayKind.CLOSEST_HIT, max_entries=10)
+    stats = hb.RayKindStats()
+    with pytest.raises(hb.CapacityExceeded):
+        hb._trace_wave(b, t, None, hb.RenderMode.LIVE, inp["primary_O"], inp["primary_D"],
+                       inp["primary_tmin"], inp["primary_tmax"], stats, closest=True,
+                       log_lists=None)
+    assert t.entry_count == 0  # the wave was not committed
+
+
+def test_empty_wave(hb):
+    b = gbvh(hb, "strip8")
+    t = hb.PredictorTable(hb.HashConfig(6), 0, hb.RayKind.HIT_ANY)
+    out, stats = hb.trace_wave(b, t, "live", np.zeros((0, 3), np.float32),
+                               np.zeros((0, 3), np.float32), np.zeros(0), np.zeros(0),
+                               closest=False)
+    assert stats.sum() == 0 and len(out["found"]) == 0
+
+
+# -- table API -------------------------------------------------------------------------
+
+def test_record_sequence_matches_reference(hb):
+    g = load_golden("record.npz")
+    t = hb.PredictorTable(hb.HashConfig(6), 0)
+    ins = t.record_batch(g["keys"], g["nodes"])
+    assert np.array_equal(ins, g["inserted"])
+    assert list(t.dump_lines()) == list(g["dump"])
+    ts = hb.table_stats(t)
+    assert [ts.entries, ts.stored_nodes, ts.max_nodes_per_entry,
+            ts.memory.total_bytes] == list(g["tstats"])
+    # second batch on the populated table (existing entries grow in place)
+    ins2 = t.record_batch(g["keys"][::-1], g["nodes"][::-1] + 100)
+    assert ins2.sum() > 0
+
+
+def test_record_semantics(hb):
+    t = hb.PredictorTable(hb.HashConfig(6), 0)
+    assert t.lookup(42) is None
+    assert t.record(42, 7) is True
+    assert t.record(42, 7) is False
+    assert t.record(42, 9) is True
+    assert list(t.lookup(42).nodes) == [7, 9]
+    for node in (5, 3, 11, 3, 5, 2):
+        t.record(1, node)
+    assert list(t.lookup(1).nodes) == [5, 3, 11, 2]
+    assert (t.entry_count, t.stored_node_count) == (2, 6)
+    t.record(0xABC, 5)
+    assert list(t.dump_lines())[0] == "000000000001 -> [5,3,11,2]"
+    cap = hb.PredictorTable(hb.HashConfig(6), 0, max_entries=2)
+    cap.record(1, 0)
+    cap.record(2, 0)
+    cap.record(1, 5)  # existing entries may still grow
+    with pytest.raises(hb.CapacityExceeded):
+        cap.record(3, 0)
+    assert cap.entry_count == 2
+
+
+def test_table_growth_many_waves(hb, oracle_mod):
+    """Index rehash and arena compaction under many record batches."""
+    rng = np.random.default_rng(8)
+    t = hb.PredictorTable(hb.HashConfig(6), 0)
+    o = oracle_mod.OracleTable(6, 0, True)
+    for _ in range(12):
+        keys = rng.integers(0, 30_000, 20_000).astype(np.uint64) * np.uint64(977)
+        nodes = rng.integers(0, 40, 20_000).astype(np.int32)
+        ins = t.record_batch(keys, nodes)
+        rc, ref = o.record_batch(keys, nodes)
+        assert rc == 0 and np.array_equal(ins, ref)
+    assert list(t.dump_lines()) == o.dump_lines()
+
+
+def test_predict_matches_reference(hb):
+    g = load_golden("predict.npz")
+    b = gbvh(hb, "soup256")
+    O, D = g["O"], g["D"]
+    n = O.shape[0]
+    base = hb.intersect_closest_batch(b, O, D, np.zeros(n), np.full(n, np.inf))
+    for pre, kind, go_up in (("c", hb.RayKind.CLOSEST_HIT, 1), ("a", hb.RayKind.HIT_ANY, 0)):
+        t = hb.PredictorTable(hb.HashConfig(4), go_up, kind)
+        keys = hb.hash_rays(O, D, t.cfg)
+        lut = b.ancestor_lut(go_up)
+        half = np.arange(n // 2)
+        sel = half[base["found"][half]]
+        t.record_batch(keys[sel], lut[base["leaf"][sel]])
+        assert list(t.dump_lines()) == list(g[f"{pre}_dump"])
+        closest = kind is hb.RayKind.CLOSEST_HIT
+        r = t.predict_batch(b, O, D, np.zeros(n), np.full(n, np.inf if closest else 6.0))
+        assert np.array_equal(r["cls"], g[f"{pre}_cls"])
+        tp = r["cls"] == 0
+        assert np.array_equal(r["t"][tp], g[f"{pre}_t"][tp])
+        assert np.array_equal(b.tri_ids[r["slot"][tp]], g[f"{pre}_tri_id"][tp])
+        assert np.array_equal(r["box"], g[f"{pre}_box"])
+        assert np.array_equal(r["est"], g[f"{pre}_est"])
+        # the per-ray API gives the same answers
+        for i in range(0, n, 97):
+            ray = hb.Ray(O[i], D[i], kind=kind, t_max=np.inf if closest else 6.0)
+            o = t.predict(b, ray)
+            code = {"true_positive": 0, "false_positive": 1, "negative": 2}
+            assert code[o.classification.value] == g[f"{pre}_cls"][i]
+            assert o.overhead.box_tests == g[f"{pre}_box"][i]
+
+
+def test_train_from_traversal_go_up(hb):
+    b = gbvh(hb, "strip8")
+    t = hb.PredictorTable(hb.HashConfig(6), 1)
+    mk = lambda i: hb.Ray(hb.vec3(2.0 * i + 0.25, 0.25, -5.0), hb.vec3(0, 0, 1))  # noqa: E731
+    h0 = hb.intersect_closest(b, mk(0), hb.TraversalCounters())
+    h1 = hb.intersect_closest(b, mk(1), hb.TraversalCounters())
+    assert t.train_from_traversal(b, 5, h0) is True
+    assert t.train_from_traversal(b, 5, h1) is False  # siblings share the parent
+    assert list(t.lookup(5).nodes) == [int(b.parent[h0.leaf_node])]
+    lut = b.ancestor_lut(99)
+    assert np.all(lut == 0)
+
+
+# -- full-size properties ----------------------------------------------------------------
+
+def test_c1_frame_vs_oracle(hb, oracle_mod):
+    """BASELINE config c1 end to end (primary, shadow, bounce waves) in limit
+    and live mode: GPU == C oracle on every output, stat and table dump."""
+    from paper_1910_01304_b200 import scenes
+    sc = scenes.make_scene("c1")
+    b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
+    ob = oracle_mod.OracleBvh(b.bmin, b.bmax, b.left, b.right, b.axis, b.first, b.count,
+                              b.parent, b.depth, b.tv0, b.tv1, b.tv2, b.tri_ids)
+    O, D = scenes.primary_rays(sc.camera, sc.spp, seed=0)
+    n = O.shape[0]
+    base = hb.intersect_closest_batch(b, O, D, np.zeros(n), np.full(n, np.inf))
+    hit, P, N = scenes.hit_frames(O, D, base["found"], base["t"], base["slot"],
+                                  scenes.slot_normals(b.tv0, b.tv1, b.tv2))
+    lights = np.broadcast_to(np.array(sc.point_lights[0]), P.shape)
+    waves = [(True, O, D, np.zeros(n), np.full(n, np.inf)),
+             (False, *scenes.shadow_rays(P, lights)),
+             (True, *scenes.cosine_bounce(P, N, seed=0))]
+    for mode in ("limit", "live"):
+        tabs = {c: hb.PredictorTable(hb.HashConfig(6), 0, hb.RayKind.CLOSEST_HIT if c
+                                     else hb.RayKind.HIT_ANY) for c in (True, False)}
+        otabs = {c: oracle_mod.OracleTable(6, 0, c) for c in (True, False)}
+        for closest, Ow, Dw, t0, t1 in waves:
+            out, st = hb.trace_wave(b, tabs[closest], mode, Ow, Dw, t0, t1, closest,
+                                    capture_outcomes=True)
+            rc, ref, rst = oracle_mod.trace_wave(ob, otabs[closest], mode, closest, Ow, Dw, t0,
+                                                 t1, capture=True)
+            assert rc == 0
+            assert np.array_equal(st, rst), (mode, closest, st, rst)
+            for k in ("found", "t", "slot", "leaf"):
+                assert np.array_equal(out[k], ref[k]), (mode, k)
+            if mode == "limit":
+                for k in ("cls", "eval_box", "pred_t", "pred_slot"):
+                    assert np.array_equal(out[f"log_{k}"], ref["log"][k]), k
+            assert list(tabs[closest].dump_lines()) == otabs[closest].dump_lines()
+
+
+def test_large_wave_properties(hb):
+    """At 1M rays: limit and live agree on the table and the hit flags, and
+    the accounting closes (TP+FP+NEG = rays, skipped <= baseline)."""
+    from paper_1910_01304_b200 import scenes
+    sc = scenes.make_scene("c1", resolution=(512, 512), spp=4)
+    b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2)
+    O, D = scenes.primary_rays(sc.camera, sc.spp, seed=1)
+    n = O.shape[0]
+    t0, t1 = np.zeros(n), np.full(n, np.inf)
+    tl = hb.PredictorTable(hb.HashConfig(6), 0)
+    tv = hb.PredictorTable(hb.HashConfig(6), 0)
+    lim, sl = hb.trace_wave(b, tl, "limit", O, D, t0, t1, True)
+    liv, sv = hb.trace_wave(b, tv, "live", O, D, t0, t1, True)
+    assert sl[1] + sl[2] + sl[3] == n and sv[1] + sv[2] + sv[3] == n
+    assert np.array_equal(sl[1:4], sv[1:4])  # same classification counts
+    assert 0 <= sl[8] <= sl[4]
+    assert np.array_equal(lim["found"], liv["found"])  # live never changes hit flags
+    assert list(tl.dump_lines()) == list(tv.dump_lines())
+    tp = sl[1]
+    assert sv[4] < sl[4] or tp == 0  # live traced fewer boxes from the root
