@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""HRPP hot-path benchmark (BASELINE.json metric, config c2 by default).
+
+A step is one frame of BASELINE config c2 through the HRPP hot path in live
+mode (predict first, full traversal only for rays that are not true
+positives, train in ray order): the 1024x1024x8 primary wave (hit-all),
+one area-light shadow ray per primary hit (hit-any) and one cosine-weighted
+diffuse bounce per primary hit (hit-all), with fresh predictor tables per
+frame.  Inputs (float32 origins/directions, float64 tmin/tmax; 335 MB for the
+primary wave alone, larger than the 126 MB L2) are resident in HBM before the
+timed region; scenes and waves are seeded synthetic stand-ins.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Rank 0 prints one JSON line.  Multi-GPU: one process per GPU (torchrun);
+each rank takes a contiguous block of every wave and its own predictor
+tables; new (key, node) records are all-gathered between waves and merged in
+ray order.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Mrays/s with HRPP prediction vs full traversal; % BVH node visits skipped"
+KINDS = ("primary", "shadow", "bounce")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--res", default=None, help="override resolution WxH (testing)")
+    ap.add_argument("--spp", type=int, default=None)
+    ap.add_argument("--precision", type=int, default=6)
+    ap.add_argument("--go-up", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=float, default=0.125,
+                    help="fraction (prefix) of every wave timed on the CPU baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--live-rounds", type=int, default=None)
+    ap.add_argument("--profile-only", action="store_true",
+                    help="setup + a few live frames, no extras (for ncu)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def make_workload(args, trace_closest=None):
+    """Scene, BVH arrays and the three waves of one frame (host numpy).
+
+    Secondary waves are spawned from the full-traversal hits of the primary
+    wave; `trace_closest(O, D)` supplies them (GPU in our arm, the oracle in
+    the reference arm) -- the result is identical either way (bit-exact)."""
+    import paper_1910_01304_b200 as hb
+    from paper_1910_01304_b200 import scenes
+    res = tuple(int(x) for x in args.res.split("x")) if args.res else None
+    sc = scenes.make_scene(args.config, resolution=res, spp=args.spp)
+    bvh = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
+    O, D = scenes.primary_rays(sc.camera, sc.spp, seed=0)
+    n = O.shape[0]
+    t0, t1 = np.zeros(n), np.full(n, np.inf)
+    base = trace_closest(bvh, O, D, t0, t1)
+    normals = scenes.slot_normals(bvh.tv0, bvh.tv1, bvh.tv2)
+    _, P, N = scenes.hit_frames(O, D, base["found"], base["t"], base["slot"], normals)
+    if sc.area_light is not None:
+        lp = scenes.area_light_samples(P.shape[0], sc.area_light[0], sc.area_light[1], seed=0)
+    else:
+        lp = np.broadcast_to(np.asarray(sc.point_lights[0], np.float64), P.shape)
+    waves = {"primary": (True, O, D, t0, t1),
+             "shadow": (False, *scenes.shadow_rays(P, lp)),
+             "bounce": (True, *scenes.cosine_bounce(P, N, seed=0))}
+    return sc, bvh, waves
+
+
+def shard(wave, rank, world):
+    """Contiguous ray block of this rank (never interleave: SURVEY 8(e))."""
+    closest, O, D, t0, t1 = wave
+    n = O.shape[0]
+    lo, hi = (n * rank) // world, (n * (rank + 1)) // world
+    return closest, O[lo:hi], D[lo:hi], t0[lo:hi], t1[lo:hi]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.proc = None
+        self.lines = []
+        self.device = device
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_1910_01304_b200 as hb
+    from paper_1910_01304_b200 import _lib
+    from paper_1910_01304_b200.parallel import merge_wave_records
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if args.live_rounds is not None:
+        hb.set_live_rounds(args.live_rounds)
+
+    def gpu_trace(bvh, O, D, t0, t1):
+        return hb.intersect_closest_batch(bvh, O, D, t0, t1)
+
+    sc, bvh, waves = make_workload(args, gpu_trace)
+    cfg = hb.HashConfig(args.precision)
+    tables = {True: hb.PredictorTable(cfg, args.go_up, hb.RayKind.CLOSEST_HIT, device=local_rank),
+              False: hb.PredictorTable(cfg, args.go_up, hb.RayKind.HIT_ANY, device=local_rank)}
+    my = {k: shard(w, rank, world) for k, w in waves.items()}
+    offsets = {k: (waves[k][1].shape[0] * rank) // world for k in KINDS}
+    dwaves = {k: (c, *(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in w[1:]))
+              for k, (c, *w) in ((k, (v[0], v)) for k, v in my.items())}
+    n_local = sum(w[1].shape[0] for w in dwaves.values())
+    n_total = sum(w[1].shape[0] for w in waves.values())
+    stream = torch.cuda.current_stream()
+
+    def frame(mode, stats=None, host=None):
+        for t in tables.values():
+            t.clear()
+        res = {}
+        for k in KINDS:
+            closest, O, D, t0, t1 = dwaves[k] if host is None else host[k]
+            st = stats[k] if stats is not None else None
+            out, st = hb.trace_wave(bvh, tables[closest] if mode != "baseline" else None, mode,
+                                    O, D, t0, t1, closest, stats=st,
+                                    outputs=None if host is None else host[k + "_out"],
+                                    defer_commit=world > 1 and mode != "baseline")
+            if world > 1 and mode != "baseline":
+                merge_wave_records(tables[closest], dist, ray_offset=offsets[k])
+            res[k] = (out, st)
+        return res
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            fn()
+        ev1.record(stream)
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    if args.profile_only:
+        for _ in range(max(1, args.warmup)):
+            frame("live")
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile_only": True, "rays": n_total}))
+        return
+
+    # ---- headline: live frames --------------------------------------------------------
+    for _ in range(args.warmup):
+        frame("live")
+    launches0 = _lib.launch_count()
+    _lib.profile_enable(True)
+    _lib.profile_read(reset=True)
+    with ClockSampler(local_rank) as clk:
+        ms_live = timed(lambda: frame("live"), args.steps)
+    prof = _lib.profile_read(reset=True)
+    _lib.profile_enable(False)
+    launches = _lib.launch_count() - launches0
+    value = n_total * args.steps / (ms_live * 1e-3) / 1e6
+
+    # stats of one live frame (identical every frame: fresh tables, same rays)
+    live_stats = {k: np.zeros(11, np.int64) for k in KINDS}
+    frame("live", stats=live_stats)
+
+    # ---- full traversal (baseline mode) and exact savings (limit mode) ---------------
+    for _ in range(2):
+        frame("baseline")
+    ms_base = timed(lambda: frame("baseline"), args.steps)
+    base_value = n_total * args.steps / (ms_base * 1e-3) / 1e6
+    lim_stats = {k: np.zeros(11, np.int64) for k in KINDS}
+    frame("limit", stats=lim_stats)
+    if world > 1:
+        for k in KINDS:
+            t = torch.from_numpy(lim_stats[k]).to(dev)
+            dist.all_reduce(t)
+            lim_stats[k] = t.cpu().numpy()
+            t = torch.from_numpy(live_stats[k]).to(dev)
+            dist.all_reduce(t)
+            live_stats[k] = t.cpu().numpy()
+
+    def pct(a, b):
+        return 100.0 * a / b if b else 0.0
+
+    savings = {k: round(pct(lim_stats[k][8], lim_stats[k][4]), 4) for k in KINDS}
+    base_boxes = sum(int(lim_stats[k][4]) for k in KINDS)
+    live_boxes = sum(int(live_stats[k][4] + live_stats[k][6]) for k in KINDS)
+    visit_reduction = 100.0 * (1.0 - live_boxes / base_boxes) if base_boxes else 0.0
+
+    # ---- roofline of the dominant stage -------------------------------------------------
+    steps = args.steps
+    per_frame = {k: (v[0] / steps, v[1] / steps) for k, v in prof.items()}
+    rays_frame = n_local
+    s_live = {i: sum(int(live_stats[k][i]) for k in KINDS) // world for i in range(11)}
+    ntp = s_live[1]
+    n_fallback = s_live[2] + s_live[3]
+    alg = {  # algorithmic bytes per frame
+        "hash": 32 * rays_frame,
+        "trace_queue": 64 * n_fallback + 32 * s_live[4] + 36 * s_live[5],
+        "consult": 72 * rays_frame + 36 * s_live[6] + 36 * s_live[7]
+                   + 32 * sum(int(tables[c].stored_node_count) for c in (True, False)),
+    }
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    stages = {}
+    for k, (ms, cnt) in per_frame.items():
+        if cnt == 0:
+            continue
+        ent = {"ms_per_frame": round(ms, 4), "launches_per_frame": cnt,
+               "share": round(ms / (ms_live / steps), 4)}
+        if k in alg and ms > 0:
+            ent["achieved_gbs"] = round(alg[k] / (ms * 1e-3) / 1e9, 2)
+        stages[k] = ent
+    dom = max((k for k in stages if k in alg), key=lambda k: stages[k]["ms_per_frame"])
+    d_ms = per_frame[dom][0] / max(1, per_frame[dom][1])  # average launch duration
+    d_bytes = alg[dom] / max(1, per_frame[dom][1])
+    traffic_path = ROOT / "profiles" / "traffic.json"
+    traffic = None
+    if traffic_path.exists():
+        traffic = json.loads(traffic_path.read_text()).get(dom)
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": round(d_bytes / (d_ms * 1e-3) / 1e9, 2),
+                "peak": peak, "unit": "GB/s",
+                "frac": round(d_bytes / (d_ms * 1e-3) / 1e9 / peak, 4), "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+
+    # ---- e2e: host buffers through the public API ------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        h2d = d2h = 0
+        for k in KINDS:
+            closest, O, D, t0, t1 = my[k]
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa
+            host[k] = (closest, pin(O), pin(D), pin(t0), pin(t1))
+            n = O.shape[0]
+            host[k + "_out"] = {"found": torch.empty(n, dtype=torch.bool).pin_memory(),
+                                "t": torch.empty(n, dtype=torch.float64).pin_memory(),
+                                "slot": torch.empty(n, dtype=torch.int32).pin_memory(),
+                                "leaf": torch.empty(n, dtype=torch.int32).pin_memory()}
+            h2d += n * 40
+            d2h += n * 17
+        frame("live", host=host)
+        barrier()
+        t0w = time.perf_counter()
+        e_steps = max(1, min(args.steps, 3))
+        for _ in range(e_steps):
+            frame("live", host=host)
+        barrier()
+        dt = time.perf_counter() - t0w
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": round(n_total * e_steps / dt / 1e6, 3), "unit": "Mrays/s",
+               "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+               "how": "pinned host arrays through trace_wave (C ABI stages H2D/D2H), wall clock"}
+
+    # ---- CPU baseline (oracle port, rank 0, N=1 only) ---------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_frame(bvh, waves, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_live / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded displaced icosphere scene + generated ray waves)",
+            "config": {"workload": f"{args.config}: {sc.n_tris} tris, "
+                                   f"{sc.camera.resolution[0]}x{sc.camera.resolution[1]} "
+                                   f"spp{sc.spp} primary + area-light shadow + diffuse bounce",
+                       "mode": "live (predict, else full traversal, train in ray order)",
+                       "rays_per_step": n_total,
+                       "rays_per_wave": {k: int(waves[k][1].shape[0]) for k in KINDS},
+                       "bvh_nodes": bvh.node_count, "bvh_max_depth": bvh.max_depth,
+                       "precision": args.precision, "go_up": args.go_up,
+                       "parallelism": f"contiguous ray blocks x{world}",
+                       "l2": "inputs > L2 (335 MB primary wave); no flush needed"},
+            "full_traversal_mrays_s": round(base_value, 3),
+            "speedup_vs_full_traversal": round(value / base_value, 4),
+            "nodes_skipped_percent": savings,
+            "live_node_visit_reduction_percent": round(visit_reduction, 3),
+            "stages": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the oracle port; reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+
+def _oracle_bvh(bvh):
+    from oracle import oracle
+    oracle.build()
+    return oracle.OracleBvh(bvh.bmin, bvh.bmax, bvh.left, bvh.right, bvh.axis, bvh.first,
+                            bvh.count, bvh.parent, bvh.depth, bvh.tv0, bvh.tv1, bvh.tv2,
+                            bvh.tri_ids)
+
+
+def cpu_reference_frame(bvh, waves, args, steps=1):
+    """Live-mode frame on a contiguous prefix sample of every wave through the
+    oracle (hrpp/tracer.py:278-340 restated in C).  The reference's live
+    consult is single-threaded by design (hrpp/tracer.py:12-15), so is this."""
+    from oracle import oracle
+    ob = _oracle_bvh(bvh)
+    frac = args.cpu_sample
+    sample = {k: tuple(a[:max(1, int(len(a) * frac))] if i else a
+                       for i, a in enumerate(w)) for k, w in waves.items()}
+    n = sum(s[1].shape[0] for s in sample.values())
+    best = None
+    for _ in range(steps):
+        tabs = {c: oracle.OracleTable(args.precision, args.go_up, c) for c in (True, False)}
+        t0 = time.perf_counter()
+        for k in KINDS:
+            closest, O, D, a, b = sample[k]
+            rc, _, _ = oracle.trace_wave(ob, tabs[closest], "live", closest, O, D, a, b,
+                                         threads=1)
+            assert rc == 0
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": round(n / best / 1e6, 4), "unit": "Mrays/s", "cores": 1, "kind": "port",
+            "sample": f"first {frac:g} of every wave of one frame ({n} rays), live mode, "
+                      f"fresh tables; C oracle (oracle/hrpp_oracle.c), 1 thread (the "
+                      f"reference's consult loop is sequential); host has {os.cpu_count()} "
+                      f"cores",
+            "seconds": round(best, 3)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle
+    import paper_1910_01304_b200 as hb  # host-side builder + generators only
+
+    def cpu_trace(bvh, O, D, t0, t1):
+        return _oracle_bvh(bvh).trace_batch(True, O, D, t0, t1, threads=0)
+
+    sc, bvh, waves = make_workload(args, cpu_trace)
+    # each step: live frame over the prefix sample (a bounded sample of the workload)
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_frame(bvh, waves, args)
+    t0 = time.perf_counter()
+    vals = []
+    for _ in range(args.steps):
+        r = cpu_reference_frame(bvh, waves, args)
+        vals.append(r["value"])
+    dt = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {"metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000 * dt / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same seeded scene and waves as our arm)", "impl": "reference",
+            "config": {"workload": f"{args.config}: {sc.n_tris} tris, prefix sample "
+                                   f"{args.cpu_sample:g} of each wave", "mode": "live"},
+            "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": 1, "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

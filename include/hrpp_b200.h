@@ -148,6 +148,17 @@ int hrpp_table_lookup(hrpp_table_t table, uint64_t key, int32_t *nodes_host, int
  * Host arrays: keys[entries], offsets[entries+1], nodes[stored]. */
 int hrpp_table_export(hrpp_table_t table, uint64_t *keys, int64_t *offsets, int32_t *nodes);
 
+/* Multi-GPU support: in deferred mode a wave does
+ * not modify the table; its append records (key, node, triggering ray index
+ * within the wave) are kept, sorted by ray index, and read with
+ * hrpp_table_pending (host or device pointers).  The caller all-gathers the
+ * records of every rank's contiguous ray block and applies them in global
+ * ray order with hrpp_table_record, which leaves every rank's table
+ * identical.  With one rank this equals the direct commit. */
+int hrpp_table_set_deferred(hrpp_table_t table, int on);
+int hrpp_table_pending(hrpp_table_t table, uint64_t *keys, int32_t *nodes, int32_t *rays,
+                       int64_t cap, int64_t *count);
+
 /* ---- predict: hrpp/predictor.py:167-192 over a batch, frozen table ------ */
 /* cls 0 TP / 1 FP / 2 NEG; t/slot/leaf/u/v of the entry result (t = inf for
  * NEG, the any-hit miss convention otherwise); box/tri/visited = overhead
@@ -168,6 +179,15 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t table, int mode, int closest,
                     const float *O, const float *D, const double *tmin, const double *tmax,
                     int64_t n, hrpp_wave_out *out, hrpp_outcome_log *log, int64_t *stats,
                     void *stream);
+
+/* Per-stage CUDA-event profiler: when enabled, each stage the library
+ * launches is bracketed by events on its own stream.  Stages (index):
+ * 0 hash, 1 full traversal batch, 2 live fallback traversal (queue),
+ * 3 grouping (radix sort by key + segment heads), 4 consult, 5 table commit,
+ * 6 other.  hrpp_profile_read synchronizes the device and returns the
+ * accumulated milliseconds and stage counts (number of stages = 7). */
+int hrpp_profile_enable(int on);
+int hrpp_profile_read(double *ms, int64_t *counts, int n, int reset);
 
 /* Live-mode speculation policy (rounds of exact per-key scan before the
  * speculative round).  Default 3.  Affects speed only, never results. */

@@ -46,6 +46,8 @@ def _load():
     L.hrpp_launch_count.restype = I64
     L.hrpp_device_count.argtypes = [P]
     L.hrpp_set_live_rounds.argtypes = [C.c_int]
+    L.hrpp_profile_enable.argtypes = [C.c_int]
+    L.hrpp_profile_read.argtypes = [P, P, C.c_int, C.c_int]
     L.hrpp_hash_rays.argtypes = [P, P, I64, C.c_int, P, P]
     L.hrpp_hash_floats.argtypes = [P, I64, C.c_int, P, P]
     L.hrpp_bvh_create.argtypes = [P] * 13 + [I64, I64, C.c_int, P]
@@ -60,6 +62,8 @@ def _load():
     L.hrpp_table_record.argtypes = [P, P, P, I64, P, P]
     L.hrpp_table_lookup.argtypes = [P, C.c_uint64, P, I64, P]
     L.hrpp_table_export.argtypes = [P, P, P, P]
+    L.hrpp_table_set_deferred.argtypes = [P, C.c_int]
+    L.hrpp_table_pending.argtypes = [P, P, P, P, I64, P]
     L.hrpp_predict_batch.argtypes = [P, P, P, P, P, P, P, I64] + [P] * 10 + [P]
     L.hrpp_trace_wave.argtypes = [P, P, C.c_int, C.c_int, P, P, P, P, I64, C.POINTER(WaveOut),
                                   C.POINTER(OutcomeLogC), P, P]
@@ -68,19 +72,50 @@ def _load():
                  "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch",
                  "hrpp_table_create", "hrpp_table_destroy", "hrpp_table_clear",
                  "hrpp_table_info", "hrpp_table_record", "hrpp_table_lookup",
-                 "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave"):
+                 "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
+                 "hrpp_profile_enable", "hrpp_profile_read", "hrpp_table_set_deferred",
+                 "hrpp_table_pending"):
         getattr(L, name).restype = C.c_int
     return L
 
 
-lib = _load()
+class _LazyLib:
+    """Loads the shared library on first use, so that importing the package
+    (e.g. to run the build) works before the library exists.  Any compute
+    call without the library raises ImportError: there is no fallback."""
+
+    _real = None
+
+    def __getattr__(self, name):
+        if _LazyLib._real is None:
+            _LazyLib._real = _load()
+        return getattr(_LazyLib._real, name)
+
+
+lib = _LazyLib()
 
 EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device_count",
             "hrpp_hash_rays", "hrpp_hash_floats", "hrpp_bvh_create", "hrpp_bvh_destroy",
             "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch", "hrpp_table_create",
             "hrpp_table_destroy", "hrpp_table_clear", "hrpp_table_info", "hrpp_table_record",
             "hrpp_table_lookup", "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
-            "hrpp_set_live_rounds")
+            "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
+            "hrpp_table_set_deferred", "hrpp_table_pending")
+
+PROFILE_STAGES = ("hash", "trace", "trace_queue", "group", "consult", "commit", "other")
+
+
+def profile_enable(on: bool = True):
+    lib.hrpp_profile_enable(int(bool(on)))
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{stage: (milliseconds, launches)} accumulated since the last reset."""
+    ms = np.zeros(len(PROFILE_STAGES), np.float64)
+    cnt = np.zeros(len(PROFILE_STAGES), np.int64)
+    lib.hrpp_profile_read(ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p),
+                          len(PROFILE_STAGES), int(bool(reset)))
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(PROFILE_STAGES)}
 
 
 def last_error() -> str:

@@ -94,6 +94,53 @@ int BvhDev::ancestor_lut(int level, const int32_t** out) {
   return 0;
 }
 
+// ---- per-stage CUDA-event profiler --------------------------------------------
+bool g_prof_on = false;
+struct ProfState {
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+  double ms[P_NCAT] = {0};
+  long long count[P_NCAT] = {0};
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+static ProfState g_prof;
+
+ProfScope::ProfScope(int c, cudaStream_t s) : cat(c), st(s) {
+  if (!g_prof_on) return;
+  a = g_prof.get();
+  b = g_prof.get();
+  cudaEventRecord(a, st);
+}
+
+ProfScope::~ProfScope() {
+  if (!a) return;
+  cudaEventRecord(b, st);
+  g_prof.pending.emplace_back(cat, a, b);
+}
+
+void prof_flush() {
+  for (auto& p : g_prof.pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(std::get<2>(p));
+    if (cudaEventElapsedTime(&ms, std::get<1>(p), std::get<2>(p)) == cudaSuccess) {
+      g_prof.ms[std::get<0>(p)] += ms;
+      g_prof.count[std::get<0>(p)] += 1;
+    }
+    g_prof.pool.push_back(std::get<1>(p));
+    g_prof.pool.push_back(std::get<2>(p));
+  }
+  g_prof.pending.clear();
+}
+
 static Workspace& global_ws() {
   static Workspace ws[64];
   int dev = 0;
@@ -173,7 +220,7 @@ static int choose_stack(int height) {
 struct Pinned {
   long long* p = nullptr;
   int get() {
-    if (!p) HRPP_CK(cudaMallocHost(&p, sizeof(long long) * 32));
+    if (!p) HRPP_CK(cudaMallocHost(&p, sizeof(long long) * 40));
     return 0;
   }
 };
@@ -203,6 +250,24 @@ int hrpp_device_count(int* count) {
   *count = 0;
   HRPP_CK(cudaGetDeviceCount(count));
   return HRPP_OK;
+}
+int hrpp_profile_enable(int on) {
+  g_prof_on = on != 0;
+  return HRPP_OK;
+}
+int hrpp_profile_read(double* ms, int64_t* counts, int n, int reset) {
+  cudaDeviceSynchronize();
+  prof_flush();
+  for (int k = 0; k < n && k < P_NCAT; k++) {
+    if (ms) ms[k] = g_prof.ms[k];
+    if (counts) counts[k] = g_prof.count[k];
+  }
+  if (reset)
+    for (int k = 0; k < P_NCAT; k++) {
+      g_prof.ms[k] = 0;
+      g_prof.count[k] = 0;
+    }
+  return P_NCAT;
 }
 int hrpp_set_live_rounds(int rounds) {
   CHECK_ARG(rounds >= 0 && rounds < 1000, "live rounds must be in [0, 1000)");
@@ -449,7 +514,8 @@ static int read_meta_and_finish(TableDev& t, int* err, cudaStream_t st, Stager& 
                                 unsigned long long* stats_dev) {
   int rc;
   if ((rc = g_pinned.get())) return rc;
-  HRPP_CK(cudaMemcpyAsync(g_pinned.p, t.meta, sizeof(long long) * 3, cudaMemcpyDeviceToHost, st));
+  HRPP_CK(cudaMemcpyAsync(g_pinned.p + 28, t.meta, sizeof(long long) * 4, cudaMemcpyDeviceToHost,
+                          st));
   HRPP_CK(cudaMemcpyAsync(g_pinned.p + 3, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (stats_dev)
     HRPP_CK(cudaMemcpyAsync(g_pinned.p + 4, stats_dev, sizeof(long long) * 16,
@@ -457,9 +523,10 @@ static int read_meta_and_finish(TableDev& t, int* err, cudaStream_t st, Stager& 
   if ((rc = sg.finish())) return rc;
   int e = *(int*)(g_pinned.p + 3);
   if (e == 0) {
-    t.n_entries = g_pinned.p[0];
-    t.stored = g_pinned.p[1];
-    t.arena_used = g_pinned.p[2];
+    t.n_entries = g_pinned.p[28];
+    t.stored = g_pinned.p[29];
+    t.arena_used = g_pinned.p[30];
+    t.pending = t.deferred ? g_pinned.p[31] : 0;
   }
   return 0;
 }
@@ -493,6 +560,31 @@ int hrpp_table_record(hrpp_table_t t, const uint64_t* keys, const int32_t* nodes
     set_error("internal error %d in record", e);
     return HRPP_CUDA;
   }
+  return HRPP_OK;
+}
+
+int hrpp_table_set_deferred(hrpp_table_t t, int on) {
+  CHECK_ARG(t, "null table");
+  t->deferred = on != 0;
+  t->pending = 0;
+  return HRPP_OK;
+}
+
+int hrpp_table_pending(hrpp_table_t t, uint64_t* keys, int32_t* nodes, int32_t* rays,
+                       int64_t cap, int64_t* count) {
+  CHECK_ARG(t && count, "null argument");
+  HRPP_CK(cudaSetDevice(t->device));
+  *count = t->pending;
+  int64_t m = t->pending < cap ? t->pending : cap;
+  if (m <= 0) return HRPP_OK;
+  void *pk, *pn, *pr;
+  int rc;
+  if ((rc = t->ws.get_raw("p_keys", 0, &pk)) || (rc = t->ws.get_raw("p_nodes", 0, &pn)) ||
+      (rc = t->ws.get_raw("p_rays", 0, &pr)))
+    return rc;
+  if (keys) HRPP_CK(cudaMemcpy(keys, pk, sizeof(uint64_t) * m, cudaMemcpyDefault));
+  if (nodes) HRPP_CK(cudaMemcpy(nodes, pn, sizeof(int32_t) * m, cudaMemcpyDefault));
+  if (rays) HRPP_CK(cudaMemcpy(rays, pr, sizeof(int32_t) * m, cudaMemcpyDefault));
   return HRPP_OK;
 }
 

@@ -101,10 +101,14 @@ struct TableDev {
   int64_t e_cap = 0;
   int32_t* arena = nullptr;
   int64_t arena_cap = 0;
-  // device meta: [0] entries, [1] stored, [2] arena_used
+  // device meta: [0] entries, [1] stored, [2] arena_used, [3] pending records
   long long* meta = nullptr;
   // host mirrors (exact after every call returns)
   int64_t n_entries = 0, stored = 0, arena_used = 0;
+  // deferred mode (multi-GPU): a wave does not commit; its append records
+  // (key, node, ray index) wait in ws "p_keys"/"p_nodes"/"p_rays", sorted by ray
+  bool deferred = false;
+  int64_t pending = 0;
   Workspace ws;
   ~TableDev();
   int reserve(int64_t extra_rays, cudaStream_t st);  // capacity for a wave of extra_rays
@@ -162,6 +166,9 @@ int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_
                  uint8_t* inserted, int* err, cudaStream_t st);
 int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
                  int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st);
+int table_collect_pending(TableDev& t, const Segments& seg, int64_t n, const int32_t* seg_napp,
+                          const int32_t* app, const int32_t* app_ray, int* err,
+                          cudaStream_t st);
 int table_export(TableDev& t, uint64_t* keys_h, int64_t* offs_h, int32_t* nodes_h);
 int table_max_len(TableDev& t, int64_t* out);
 int table_lookup1(TableDev& t, uint64_t key, int32_t* nodes_h, int64_t cap, int64_t* len);
@@ -180,5 +187,17 @@ inline int grid_for(int64_t n, int block, int max_blocks) {
 }
 
 int num_sms();
+
+// ---- optional per-stage CUDA-event profiler (hrpp_profile_*) ----
+enum ProfCat { P_HASH = 0, P_TRACE, P_TRACE_QUEUE, P_GROUP, P_CONSULT, P_COMMIT, P_OTHER, P_NCAT };
+extern bool g_prof_on;
+struct ProfScope {
+  int cat;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int c, cudaStream_t s);
+  ~ProfScope();
+};
+void prof_flush();
 
 }  // namespace hrpp

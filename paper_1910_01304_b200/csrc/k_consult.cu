@@ -51,6 +51,7 @@ struct ConsultArgs {
   int32_t* seg_napp;
   int32_t* seg_cursor;
   int32_t* app;
+  int32_t* app_ray;  // ray index that triggered each append (deferred mode)
   // full-traversal results by ray index (baseline in limit mode)
   const uint8_t* f_found;
   const double* f_t;
@@ -251,7 +252,11 @@ __global__ void __launch_bounds__(128) k_consult(ConsultArgs a) {
         const int32_t cf = __shfl_sync(kFull, c, f);
         const bool inLf = __shfl_sync(kFull, inL, f);
         if (cf >= 0 && !inLf) {  // record(key, anc[leaf]) grows the entry
-          if (lane == 0) app[napp] = cf;
+          const int32_t rf = __shfl_sync(kFull, idx, f);
+          if (lane == 0) {
+            app[napp] = cf;
+            a.app_ray[beg + napp] = rf;
+          }
           __syncwarp();
           napp++;
           L++;
@@ -311,6 +316,7 @@ static void dispatch_consult(int stack, int grid, cudaStream_t st, const Consult
 
 static void launch_consult(bool closest, bool live, int stack, int grid, cudaStream_t st,
                            const ConsultArgs& a) {
+  ProfScope ps(P_CONSULT, st);
   if (closest) {
     if (live) dispatch_consult<true, true>(stack, grid, st, a);
     else dispatch_consult<true, false>(stack, grid, st, a);
@@ -356,6 +362,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   if ((rc = ws.get("k_napp", n, &a.seg_napp))) return rc;
   if ((rc = ws.get("k_cursor", n, &a.seg_cursor))) return rc;
   if ((rc = ws.get("k_app", n, &a.app))) return rc;
+  if ((rc = ws.get("k_appray", n, &a.app_ray))) return rc;
   if ((rc = ws.get("k_work", 1, &a.work))) return rc;
   const int grid = num_sms() * 8;
   if (!c.live) {
@@ -433,6 +440,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
                                                                  a.seg_cursor, err);
     HRPP_LAUNCHED();
   }
+  if (t.deferred)
+    return table_collect_pending(t, seg, n, a.seg_napp, a.app, a.app_ray, err, st);
   return table_commit(t, seg, n, a.seg_eid, a.seg_napp, a.app, err, st);
 }
 

@@ -80,6 +80,7 @@ int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys
   if (n <= 0) return 0;
   int64_t nq = (n + 3) / 4;
   int grid = grid_for(nq, 256, num_sms() * 8);
+  ProfScope ps(P_HASH, st);
   k_hash<<<grid, 256, 0, st>>>(O, D, n, p, keys, err);
   HRPP_LAUNCHED();
   return 0;
@@ -179,6 +180,7 @@ int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
   if (n <= 0) return 0;
   TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
   int grid = (int)((n + 127) / 128);
+  ProfScope ps(ray_idx ? P_TRACE_QUEUE : P_TRACE, st);
   if (closest) dispatch_trace<true>(b.stack, grid, st, a);
   else dispatch_trace<false>(b.stack, grid, st, a);
   HRPP_LAUNCHED();

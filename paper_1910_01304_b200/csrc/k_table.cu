@@ -46,6 +46,7 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
   if ((rc = ws.get("g_segstart", n + 1, &seg->seg_start))) return rc;
   if ((rc = ws.get("g_nsegs", 1, &seg->nsegs))) return rc;
   int grid = grid_for(n, 256, num_sms() * 8);
+  ProfScope ps(P_GROUP, st);
   k_iota<<<grid, 256, 0, st>>>(iota, n);
   HRPP_LAUNCHED();
   const unsigned long long* kin = reinterpret_cast<const unsigned long long*>(keys);
@@ -301,6 +302,7 @@ int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
   if ((rc = t.ws.get("m_scan", n, &scan))) return rc;
   if ((rc = t.ws.get("m_tot", 4, &totals))) return rc;
   int grid = grid_for(n, 256, num_sms() * 8);
+  ProfScope ps(P_COMMIT, st);
   k_commit_prepare<<<grid, 256, 0, st>>>(seg.nsegs, n, seg_eid, seg_napp, t.e_len, vals, err);
   HRPP_LAUNCHED();
   size_t b = 0;
@@ -316,6 +318,94 @@ int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
                                        t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, err);
   HRPP_LAUNCHED();
   k_commit_finish<<<1, 1, 0, st>>>(t.meta, totals, err);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// deferred mode: gather the wave's append records, sorted by ray index
+// ---------------------------------------------------------------------------
+
+__global__ void k_pend_count(const int* nsegs, int64_t n, const int32_t* __restrict__ seg_napp,
+                             long long* cnt, const int* err) {
+  const int ns = *nsegs;
+  const bool dead = *err != 0;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x)
+    cnt[s] = (s < ns && !dead) ? seg_napp[s] : 0;
+}
+
+__global__ void k_pend_scatter(const int* nsegs, const int32_t* __restrict__ seg_start,
+                               const unsigned long long* __restrict__ skeys,
+                               const int32_t* __restrict__ seg_napp,
+                               const int32_t* __restrict__ app,
+                               const int32_t* __restrict__ app_ray,
+                               const long long* __restrict__ off, unsigned long long* pk,
+                               int32_t* pn, int32_t* pr, int32_t* iota, const int* err) {
+  if (*err) return;
+  const int ns = *nsegs;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+    const int32_t napp = seg_napp[s], b = seg_start[s];
+    const long long o = off[s];
+    for (int32_t j = 0; j < napp; j++) {
+      pk[o + j] = skeys[b];
+      pn[o + j] = app[b + j];
+      pr[o + j] = app_ray[b + j];
+      iota[o + j] = (int32_t)(o + j);
+    }
+  }
+}
+
+__global__ void k_pend_total(const long long* cnt, const long long* off, int64_t n,
+                             long long* meta) {
+  meta[3] = off[n - 1] + cnt[n - 1];
+}
+
+__global__ void k_pend_gather(const int32_t* __restrict__ perm, const long long* meta,
+                              const unsigned long long* __restrict__ pk,
+                              const int32_t* __restrict__ pn, unsigned long long* ok,
+                              int32_t* on) {
+  const long long m = meta[3];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    ok[i] = pk[perm[i]];
+    on[i] = pn[perm[i]];
+  }
+}
+
+int table_collect_pending(TableDev& t, const Segments& seg, int64_t n, const int32_t* seg_napp,
+                          const int32_t* app, const int32_t* app_ray, int* err,
+                          cudaStream_t st) {
+  long long *cnt, *off;
+  unsigned long long *pk, *okeys;
+  int32_t *pn, *pr, *iota, *rays_sorted, *perm, *onodes;
+  int rc;
+  if ((rc = t.ws.get("q_cnt", n, &cnt)) || (rc = t.ws.get("q_off", n, &off)) ||
+      (rc = t.ws.get("q_pk", n, &pk)) || (rc = t.ws.get("q_pn", n, &pn)) ||
+      (rc = t.ws.get("q_pr", n, &pr)) || (rc = t.ws.get("q_iota", n, &iota)) ||
+      (rc = t.ws.get("p_rays", n, &rays_sorted)) || (rc = t.ws.get("q_perm", n, &perm)) ||
+      (rc = t.ws.get("p_keys", n, &okeys)) || (rc = t.ws.get("p_nodes", n, &onodes)))
+    return rc;
+  int grid = grid_for(n, 256, num_sms() * 8);
+  ProfScope ps(P_COMMIT, st);
+  HRPP_CK(cudaMemsetAsync(pr, 0x7F, sizeof(int32_t) * n, st));  // pad rays sort last
+  k_pend_count<<<grid, 256, 0, st>>>(seg.nsegs, n, seg_napp, cnt, err);
+  HRPP_LAUNCHED();
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b1, cnt, off, (int)n, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, pr, rays_sorted, iota, perm, (int)n, 0, 32, st);
+  void* tmp;
+  if ((rc = t.ws.get_raw("q_tmp", b1 > b2 ? b1 : b2, &tmp))) return rc;
+  HRPP_CK(cub::DeviceScan::ExclusiveSum(tmp, b1, cnt, off, (int)n, st));
+  k_pend_scatter<<<grid, 256, 0, st>>>(seg.nsegs, seg.seg_start, seg.skeys, seg_napp, app,
+                                       app_ray, off, pk, pn, pr, iota, err);
+  HRPP_LAUNCHED();
+  k_pend_total<<<1, 1, 0, st>>>(cnt, off, n, t.meta);
+  HRPP_LAUNCHED();
+  // ray indices are < 2^31, padding 0x7F7F7F7F sorts after every real record
+  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b2, pr, rays_sorted, iota, perm, (int)n, 0, 32,
+                                          st));
+  k_pend_gather<<<grid, 256, 0, st>>>(perm, t.meta, pk, pn, okeys, onodes);
   HRPP_LAUNCHED();
   return 0;
 }

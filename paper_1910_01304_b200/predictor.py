@@ -210,6 +210,31 @@ class PredictorTable:
         for i, k in enumerate(keys):
             yield int(k), PredictorEntry(nodes[offs[i]:offs[i + 1]])
 
+    # -- multi-GPU record exchange -------------------------------
+
+    def set_deferred(self, on: bool):
+        """In deferred mode a wave leaves the table unchanged and keeps its
+        append records for ``pending_records`` (see parallel.py)."""
+        on = bool(on)
+        if getattr(self, "_deferred", False) != on:
+            _lib.check(_lib.lib.hrpp_table_set_deferred(self.handle, int(on)), "set_deferred")
+            self._deferred = on
+
+    def pending_records(self):
+        """(keys u64, nodes i32, ray indices i32) of the last deferred wave,
+        sorted by ray index within the wave."""
+        cnt = C.c_int64()
+        _lib.check(_lib.lib.hrpp_table_pending(self.handle, None, None, None, 0, C.byref(cnt)),
+                   "pending")
+        m = cnt.value
+        keys = np.empty(m, np.uint64)
+        nodes = np.empty(m, np.int32)
+        rays = np.empty(m, np.int32)
+        if m:
+            _lib.check(_lib.lib.hrpp_table_pending(self.handle, _lib.ptr(keys), _lib.ptr(nodes),
+                                                   _lib.ptr(rays), m, C.byref(cnt)), "pending")
+        return keys, nodes, rays
+
     def clear(self):
         if self._handle is not None:
             _lib.check(_lib.lib.hrpp_table_clear(self._handle), "clear")

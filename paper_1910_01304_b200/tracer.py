@@ -63,7 +63,8 @@ def set_live_rounds(rounds: int):
 
 def trace_wave(bvh: Bvh, table: Optional[PredictorTable], mode: RenderMode, O, D, tmins,
                tmaxs, closest: bool, stats: Optional[np.ndarray] = None,
-               capture_outcomes: bool = False, want_keys: bool = False, outputs=None):
+               capture_outcomes: bool = False, want_keys: bool = False, outputs=None,
+               defer_commit: bool = False):
     """Run one wave.  Returns (result dict, stats int64[11]).
 
     Result keys: found, t, slot, leaf (+ u, v (closest), box, tri, visited in
@@ -77,6 +78,8 @@ def trace_wave(bvh: Bvh, table: Optional[PredictorTable], mode: RenderMode, O, D
             raise ValueError(f"{mode.value} mode needs a predictor table")
         if table.closest != bool(closest):
             raise ValueError("table kind does not match the wave's ray kind")
+    if table is not None and mode is not RenderMode.BASELINE:
+        table.set_deferred(defer_commit)
     O = _lib.as_array(O, np.float32, shape=(-1, 3))
     D = _lib.as_array(D, np.float32, shape=(-1, 3))
     n = int(O.shape[0])

@@ -424,3 +424,37 @@ def test_large_wave_properties(hb):
     assert list(tl.dump_lines()) == list(tv.dump_lines())
     tp = sl[1]
     assert sv[4] < sl[4] or tp == 0  # live traced fewer boxes from the root
+
+
+def test_deferred_commit_equals_direct_and_two_block_merge(hb):
+    """Deferred wave + record_batch(pending) == direct commit (one rank), and a
+    two-rank contiguous-block emulation leaves both tables identical."""
+    from paper_1910_01304_b200.parallel import block_range, merge_records
+    inp = load_golden("wave_inputs.npz")
+    b = gbvh(hb, "spheres")
+    args = [inp[f"primary_{k}"] for k in ("O", "D", "tmin", "tmax")]
+    ta = hb.PredictorTable(hb.HashConfig(6), 0)
+    tb = hb.PredictorTable(hb.HashConfig(6), 0)
+    oa, sa = hb.trace_wave(b, ta, "live", *args, closest=True)
+    ob, sb = hb.trace_wave(b, tb, "live", *args, closest=True, defer_commit=True)
+    assert tb.entry_count == 0
+    k, nd, r = tb.pending_records()
+    assert np.all(np.diff(r) > 0)
+    tb.record_batch(k, nd)
+    assert list(ta.dump_lines()) == list(tb.dump_lines())
+    assert np.array_equal(sa, sb) and np.array_equal(oa["t"], ob["t"])
+    # two contiguous blocks, consulted independently, merged in ray order
+    n = args[0].shape[0]
+    tabs = [hb.PredictorTable(hb.HashConfig(6), 0) for _ in range(2)]
+    parts = []
+    for rank in range(2):
+        lo, hi = block_range(n, rank, 2)
+        hb.trace_wave(b, tabs[rank], "live", *(a[lo:hi] for a in args), closest=True,
+                      defer_commit=True)
+        parts.append((*tabs[rank].pending_records(), lo))
+    mk, mn = merge_records([p[0] for p in parts], [p[1] for p in parts],
+                           [p[2] for p in parts], [p[3] for p in parts])
+    for t in tabs:
+        t.record_batch(mk, mn)
+    assert list(tabs[0].dump_lines()) == list(tabs[1].dump_lines())
+    assert tabs[0].entry_count == ta.entry_count  # table_entries is order-independent
