@@ -183,8 +183,9 @@ def run_ours(args, rank, world, local_rank):
               False: hb.PredictorTable(cfg, args.go_up, hb.RayKind.HIT_ANY, device=local_rank)}
     my = {k: shard(w, rank, world) for k, w in waves.items()}
     offsets = {k: (waves[k][1].shape[0] * rank) // world for k in KINDS}
-    dwaves = {k: (c, *(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in w[1:]))
-              for k, (c, *w) in ((k, (v[0], v)) for k, v in my.items())}
+    dwaves = {}
+    for k, (closest, *arrs) in my.items():
+        dwaves[k] = (closest, *(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs))
     n_local = sum(w[1].shape[0] for w in dwaves.values())
     n_total = sum(w[1].shape[0] for w in waves.values())
     stream = torch.cuda.current_stream()

@@ -251,6 +251,11 @@ int hrpp_device_count(int* count) {
   HRPP_CK(cudaGetDeviceCount(count));
   return HRPP_OK;
 }
+int hrpp_set_consult_short(int len) {
+  CHECK_ARG(len >= 0, "short segment length must be >= 0");
+  g_consult_short = len;
+  return HRPP_OK;
+}
 int hrpp_profile_enable(int on) {
   g_prof_on = on != 0;
   return HRPP_OK;

@@ -133,6 +133,10 @@ struct Segments {
 };
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
                  cudaStream_t st);
+// indices i < n with flags[i] != 0, ascending, count to *count_dev
+int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, int* count_dev,
+                  cudaStream_t st);
+extern int g_consult_short;
 
 struct Consult {
   bool live = false;

@@ -78,7 +78,7 @@ struct ConsultArgs {
   double* log_pred_t;
   int64_t* log_pred_slot;
   unsigned long long* stats;
-  int* work;
+  uint8_t* need;  // live: rays whose full traversal the consult needs next
   int32_t* queue;
   int* qcount;
   int spec;  // 0: enqueue the first unknown ray; 2: enqueue every unresolved ray
@@ -87,14 +87,7 @@ struct ConsultArgs {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ void enqueue(const ConsultArgs& a, bool enq, int32_t idx, int lane) {
-  unsigned em = __ballot_sync(kFull, enq);
-  if (!em) return;
-  int base = 0;
-  if (lane == 0) base = atomicAdd(a.qcount, __popc(em));
-  base = __shfl_sync(kFull, base, 0);
-  if (enq) a.queue[base + __popc(em & ((1u << lane) - 1u))] = idx;
-}
+int g_consult_short = 8;  // segments up to this many rays run one lane each
 
 __device__ __forceinline__ Ray load_ray(const ConsultArgs& a, bool valid, int32_t idx) {
   if (valid) return make_ray(a.O, a.D, a.tmin, a.tmax, idx);
@@ -126,159 +119,253 @@ __device__ __forceinline__ void store_state(const ConsultArgs& a, int32_t pos, c
   a.s_tri[pos] = acc.tris;
 }
 
+struct Tally {
+  long long tp = 0, fp = 0, neg = 0, ob = 0, ot = 0, sk = 0, est = 0, wr = 0, bb = 0, bt = 0;
+};
+
+// The entry's j-th node: stored list first, then this wave's appends.
+__device__ __forceinline__ int32_t entry_node(const ConsultArgs& a, int64_t ex_off,
+                                              int32_t ex_len, const int32_t* app, int32_t j) {
+  return j < ex_len ? a.arena[ex_off + j] : app[j - ex_len];
+}
+
+// Fold entry nodes [from, L) into acc: eval_entry_{closest,any}, resumable.
+template <bool CLOSEST, int STACK>
+__device__ __noinline__ void catch_up(const ConsultArgs& a, const Ray& r, Hit& acc, int32_t from,
+                                      int32_t L, int64_t ex_off, int32_t ex_len,
+                                      const int32_t* app) {
+  for (int32_t j = from; j < L; j++) {
+    if (!CLOSEST && acc.found) break;  // eval_entry_any stops at the first hit
+    fold_entry<CLOSEST>(acc, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r,
+                                                        entry_node(a, ex_off, ex_len, app, j)));
+  }
+}
+
+template <bool CLOSEST, bool LIVE>
+__device__ __forceinline__ void commit_tp(const ConsultArgs& a, Tally& c, int32_t idx,
+                                          const Hit& acc) {
+  c.tp++;
+  c.ob += acc.boxes;
+  c.ot += acc.tris;
+  const int64_t x = (int64_t)a.depth[acc.leaf] + 1 - acc.boxes;
+  c.est += x > 0 ? x : 0;
+  if (LIVE) {
+    a.o_found[idx] = 1;
+    a.o_t[idx] = acc.t;
+    a.o_slot[idx] = acc.slot;
+    a.o_leaf[idx] = acc.leaf;
+  } else {
+    c.sk += a.f_box[idx] - acc.boxes;
+    if (CLOSEST && acc.t > a.f_t[idx] + kWrongClosestEps) c.wr++;
+    if (a.log_cls) {
+      a.log_cls[idx] = 0;
+      a.log_eval_box[idx] = acc.boxes;
+      a.log_pred_t[idx] = acc.t;
+      a.log_pred_slot[idx] = acc.slot;
+    }
+  }
+}
+
+template <bool LIVE>
+__device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int32_t idx,
+                                            const Hit& acc, bool neg) {
+  if (neg) c.neg++;
+  else c.fp++;
+  c.ob += acc.boxes;
+  c.ot += acc.tris;
+  if (LIVE) {
+    const bool ff = a.f_found[idx];
+    c.bb += a.f_box[idx];
+    c.bt += a.f_tri[idx];
+    a.o_found[idx] = ff;
+    a.o_t[idx] = ff ? a.f_t[idx] : 0.0;
+    a.o_slot[idx] = ff ? a.f_slot[idx] : -1;
+    a.o_leaf[idx] = ff ? a.f_leaf[idx] : -1;
+  } else if (a.log_cls) {
+    a.log_cls[idx] = neg ? 2 : 1;
+    a.log_eval_box[idx] = acc.boxes;
+    a.log_pred_t[idx] = __longlong_as_double(0x7ff0000000000000LL);
+    a.log_pred_slot[idx] = -1;
+  }
+}
+
+// Speculative round: every not-yet-TP ray of the rest of the segment gets its
+// full traversal (TP status only grows with the entry, so after this round
+// every ray that can still need a full result has one).
+template <bool CLOSEST, int STACK>
+__device__ void speculate_rest(const ConsultArgs& a, int32_t from, int32_t end, int32_t L,
+                               int64_t ex_off, int32_t ex_len, const int32_t* app) {
+  for (int32_t j = from; j < end; j++) {
+    const int32_t idx = a.sidx[j];
+    const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+    Hit acc = empty_entry_result(CLOSEST);
+    int32_t applied = 0;
+    load_state(a, j, acc, applied);
+    catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+    store_state(a, j, acc, L);
+    if (!(L > 0 && acc.found) && !a.f_known[idx]) a.need[idx] = 1;
+  }
+}
+
+// One short key segment, replayed by one lane (hrpp/tracer.py:233-267 or
+// :295-331 restricted to one key).
 template <bool CLOSEST, bool LIVE, int STACK>
-__global__ void __launch_bounds__(128) k_consult(ConsultArgs a) {
-  if (*a.err) return;
-  const int lane = threadIdx.x & 31;
-  const int ns = *a.nsegs;
-  long long c_tp = 0, c_fp = 0, c_neg = 0, c_ob = 0, c_ot = 0, c_sk = 0, c_est = 0, c_wr = 0,
-            c_bb = 0, c_bt = 0;
-  for (;;) {
-    int s = 0;
-    if (lane == 0) s = atomicAdd(a.work, 1);
-    s = __shfl_sync(kFull, s, 0);
-    if (s >= ns) break;
-    const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
-    int32_t tb = beg, napp = 0;
-    if (LIVE) {
-      tb = a.seg_cursor[s];
-      if (tb >= end) continue;
-      napp = a.seg_napp[s];
+__device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, int32_t end,
+                           int32_t cur) {
+  const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
+  const int64_t ex_off = eid >= 0 ? a.e_off[eid] : 0;
+  const int32_t ex_len = eid >= 0 ? a.e_len[eid] : 0;
+  int32_t* app = a.app + beg;
+  int32_t napp = LIVE ? a.seg_napp[s] : 0;
+  int32_t j = cur;
+  for (; j < end; j++) {
+    const int32_t idx = a.sidx[j];
+    const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+    Hit acc = empty_entry_result(CLOSEST);
+    int32_t applied = 0;
+    if (LIVE) load_state(a, j, acc, applied);
+    const int32_t L = ex_len + napp;
+    catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+    if (L > 0 && acc.found) {
+      commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+      continue;
     }
-    const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
-    const int64_t ex_off = eid >= 0 ? a.e_off[eid] : 0;
-    const int32_t ex_len = eid >= 0 ? a.e_len[eid] : 0;
-    int32_t* app = a.app + beg;
-    bool suspended = false;
-    while (tb < end) {
-      const int32_t pos = tb + lane;
-      const bool valid = pos < end;
-      const int32_t idx = valid ? a.sidx[pos] : 0;
-      const Ray r = load_ray(a, valid, idx);
-      Hit acc = empty_entry_result(CLOSEST);
-      int32_t applied = 0;
-      if (LIVE && valid) load_state(a, pos, acc, applied);
-      int32_t L = ex_len + napp;
-      const bool fknown = valid && (!LIVE || a.f_known[idx]);
-      int32_t c = -1;
-      if (fknown && a.f_found[idx]) c = a.anc[a.f_leaf[idx]];
-      bool inL = false;
-      // bring every lane up to date with the current entry (and test
-      // whether the lane's training node is already stored)
-      for (int32_t j = 0; j < L; j++) {
-        const int32_t nd = j < ex_len ? a.arena[ex_off + j] : app[j - ex_len];
-        inL |= nd == c;
-        if (valid && j >= applied && (CLOSEST || !acc.found))
-          fold_entry<CLOSEST>(acc, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, nd));
-      }
-      applied = L;
-      int cursor = 0;
-      for (;;) {
-        const bool need = valid && lane >= cursor && (L == 0 || !acc.found);
-        const unsigned m = __ballot_sync(kFull, need);
-        const int f = m ? __ffs(m) - 1 : 32;
-        if (valid && lane >= cursor && lane < f) {  // true positives
-          c_tp++;
-          c_ob += acc.boxes;
-          c_ot += acc.tris;
-          const int64_t x = (int64_t)a.depth[acc.leaf] + 1 - acc.boxes;
-          c_est += x > 0 ? x : 0;
-          if (LIVE) {
-            a.o_found[idx] = 1;
-            a.o_t[idx] = acc.t;
-            a.o_slot[idx] = acc.slot;
-            a.o_leaf[idx] = acc.leaf;
-          } else {
-            c_sk += a.f_box[idx] - acc.boxes;
-            if (CLOSEST && acc.t > a.f_t[idx] + kWrongClosestEps) c_wr++;
-            if (a.log_cls) {
-              a.log_cls[idx] = 0;
-              a.log_eval_box[idx] = acc.boxes;
-              a.log_pred_t[idx] = acc.t;
-              a.log_pred_slot[idx] = acc.slot;
-            }
-          }
-        }
-        if (f == 32) break;
-        if (LIVE && !__shfl_sync(kFull, fknown, f)) {
-          // suspend: the full traversal of ray f is not known yet
-          enqueue(a, (lane == f) || (a.spec >= 1 && need && !fknown), idx, lane);
-          if (valid && lane >= f) store_state(a, pos, acc, applied);
-          if (a.spec >= 2) {
-            for (int32_t t2 = tb + 32; t2 < end; t2 += 32) {
-              const int32_t p2 = t2 + lane;
-              const bool v2 = p2 < end;
-              const int32_t i2 = v2 ? a.sidx[p2] : 0;
-              const Ray r2 = load_ray(a, v2, i2);
-              Hit a2 = empty_entry_result(CLOSEST);
-              int32_t ap2 = 0;
-              if (v2) load_state(a, p2, a2, ap2);
-              for (int32_t j = 0; j < L; j++) {
-                const int32_t nd = j < ex_len ? a.arena[ex_off + j] : app[j - ex_len];
-                if (v2 && j >= ap2 && (CLOSEST || !a2.found))
-                  fold_entry<CLOSEST>(a2, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r2, nd));
-              }
-              if (v2) store_state(a, p2, a2, L);
-              enqueue(a, v2 && (L == 0 || !a2.found) && !a.f_known[i2], i2, lane);
-            }
-          }
-          if (lane == 0) {
-            a.seg_cursor[s] = tb + f;
-            a.seg_napp[s] = napp;
-          }
-          suspended = true;
-          break;
-        }
-        if (lane == f) {  // NEG (no entry yet) or FP
-          if (L == 0) c_neg++;
-          else c_fp++;
-          c_ob += acc.boxes;
-          c_ot += acc.tris;
-          if (LIVE) {
-            const bool ff = a.f_found[idx];
-            c_bb += a.f_box[idx];
-            c_bt += a.f_tri[idx];
-            a.o_found[idx] = ff;
-            a.o_t[idx] = ff ? a.f_t[idx] : 0.0;
-            a.o_slot[idx] = ff ? a.f_slot[idx] : -1;
-            a.o_leaf[idx] = ff ? a.f_leaf[idx] : -1;
-          } else if (a.log_cls) {
-            a.log_cls[idx] = L == 0 ? 2 : 1;
-            a.log_eval_box[idx] = acc.boxes;
-            a.log_pred_t[idx] = __longlong_as_double(0x7ff0000000000000LL);
-            a.log_pred_slot[idx] = -1;
-          }
-        }
-        const int32_t cf = __shfl_sync(kFull, c, f);
-        const bool inLf = __shfl_sync(kFull, inL, f);
-        if (cf >= 0 && !inLf) {  // record(key, anc[leaf]) grows the entry
-          const int32_t rf = __shfl_sync(kFull, idx, f);
-          if (lane == 0) {
-            app[napp] = cf;
-            a.app_ray[beg + napp] = rf;
-          }
-          __syncwarp();
-          napp++;
-          L++;
-          inL |= c == cf;
-          if (valid && lane > f && (CLOSEST || !acc.found))
-            fold_entry<CLOSEST>(acc, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, cf));
-          applied = L;
-        }
-        cursor = f + 1;
-      }
-      if (suspended) break;
-      tb += 32;
+    if (LIVE && !a.f_known[idx]) {  // suspend until its full traversal is known
+      a.need[idx] = 1;
+      store_state(a, j, acc, L);
+      if (a.spec >= 2) speculate_rest<CLOSEST, STACK>(a, j + 1, end, L, ex_off, ex_len, app);
+      break;
     }
-    if (lane == 0) {
-      a.seg_eid[s] = eid;
-      if (!suspended) {
-        a.seg_napp[s] = napp;
-        if (LIVE) a.seg_cursor[s] = end;
+    commit_miss<LIVE>(a, c, idx, acc, L == 0);
+    if (a.f_found[idx]) {  // record(key, anc[leaf]), de-duplicated
+      const int32_t node = a.anc[a.f_leaf[idx]];
+      bool dup = false;
+      for (int32_t k = 0; k < L && !dup; k++) dup = entry_node(a, ex_off, ex_len, app, k) == node;
+      if (!dup) {
+        app[napp] = node;
+        a.app_ray[beg + napp] = idx;
+        napp++;
       }
     }
   }
-  long long v[10] = {c_tp, c_fp, c_neg, c_bb, c_bt, c_ob, c_ot, c_sk, c_est, c_wr};
+  if (LIVE) a.seg_cursor[s] = j;
+  a.seg_napp[s] = napp;
+  a.seg_eid[s] = eid;
+}
+
+// One long key segment, replayed by the whole warp: lanes hold 32
+// consecutive rays; a ballot finds the next non-TP ray.
+template <bool CLOSEST, bool LIVE, int STACK>
+__device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
+  const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
+  int32_t tb = LIVE ? a.seg_cursor[s] : beg;
+  int32_t napp = LIVE ? a.seg_napp[s] : 0;
+  const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
+  const int64_t ex_off = eid >= 0 ? a.e_off[eid] : 0;
+  const int32_t ex_len = eid >= 0 ? a.e_len[eid] : 0;
+  int32_t* app = a.app + beg;
+  bool suspended = false;
+  while (tb < end) {
+    const int32_t pos = tb + lane;
+    const bool valid = pos < end;
+    const int32_t idx = valid ? a.sidx[pos] : 0;
+    const Ray r = load_ray(a, valid, idx);
+    Hit acc = empty_entry_result(CLOSEST);
+    int32_t applied = 0;
+    if (LIVE && valid) load_state(a, pos, acc, applied);
+    int32_t L = ex_len + napp;
+    const bool fknown = valid && (!LIVE || a.f_known[idx]);
+    int32_t cnode = -1;
+    if (fknown && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
+    bool inL = false;
+    for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
+    if (valid) catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+    applied = L;
+    int cursor = 0;
+    for (;;) {
+      const bool need = valid && lane >= cursor && (L == 0 || !acc.found);
+      const unsigned m = __ballot_sync(kFull, need);
+      const int f = m ? __ffs(m) - 1 : 32;
+      if (valid && lane >= cursor && lane < f) commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+      if (f == 32) break;
+      if (LIVE && !__shfl_sync(kFull, fknown, f)) {  // suspend at ray f
+        if (lane == f || (a.spec >= 1 && need && !fknown)) a.need[idx] = 1;
+        if (valid && lane >= f) store_state(a, pos, acc, applied);
+        if (a.spec >= 2) {
+          for (int32_t t2 = tb + 32 + lane; t2 < end; t2 += 32) {
+            const int32_t i2 = a.sidx[t2];
+            const Ray r2 = make_ray(a.O, a.D, a.tmin, a.tmax, i2);
+            Hit a2 = empty_entry_result(CLOSEST);
+            int32_t ap2 = 0;
+            load_state(a, t2, a2, ap2);
+            catch_up<CLOSEST, STACK>(a, r2, a2, ap2, L, ex_off, ex_len, app);
+            store_state(a, t2, a2, L);
+            if (!(L > 0 && a2.found) && !a.f_known[i2]) a.need[i2] = 1;
+          }
+        }
+        if (lane == 0) {
+          a.seg_cursor[s] = tb + f;
+          a.seg_napp[s] = napp;
+        }
+        suspended = true;
+        break;
+      }
+      if (lane == f) commit_miss<LIVE>(a, c, idx, acc, L == 0);
+      const int32_t cf = __shfl_sync(kFull, cnode, f);
+      const bool inLf = __shfl_sync(kFull, inL, f);
+      if (cf >= 0 && !inLf) {  // record(key, anc[leaf]) grows the entry
+        const int32_t rf = __shfl_sync(kFull, idx, f);
+        if (lane == 0) {
+          app[napp] = cf;
+          a.app_ray[beg + napp] = rf;
+        }
+        __syncwarp();
+        napp++;
+        L++;
+        inL |= cnode == cf;
+        if (valid && lane > f) catch_up<CLOSEST, STACK>(a, r, acc, L - 1, L, ex_off, ex_len, app);
+        applied = L;
+      }
+      cursor = f + 1;
+    }
+    if (suspended) break;
+    tb += 32;
+  }
+  if (lane == 0) {
+    a.seg_eid[s] = eid;
+    if (!suspended) {
+      a.seg_napp[s] = napp;
+      if (LIVE) a.seg_cursor[s] = end;
+    }
+  }
+}
+
+// Thread t owns key segment t; segments longer than `short_len` rays are
+// replayed cooperatively by the owning warp.  No global work queue.
+template <bool CLOSEST, bool LIVE, int STACK>
+__global__ void __launch_bounds__(128) k_consult(ConsultArgs a, int short_len) {
+  if (*a.err) return;
+  const int lane = threadIdx.x & 31;
+  const int ns = *a.nsegs;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  Tally c;
+  bool active = false, small = false;
+  int32_t beg = 0, end = 0, cur = 0;
+  if (s < ns) {
+    beg = a.seg_start[s];
+    end = a.seg_start[s + 1];
+    cur = LIVE ? a.seg_cursor[s] : beg;
+    active = cur < end;
+    small = end - beg <= short_len;
+  }
+  if (active && small) seg_thread<CLOSEST, LIVE, STACK>(a, c, s, beg, end, cur);
+  unsigned lm = __ballot_sync(kFull, active && !small);
+  while (lm) {
+    const int l = __ffs(lm) - 1;
+    lm &= lm - 1;
+    seg_warp<CLOSEST, LIVE, STACK>(a, c, __shfl_sync(kFull, s, l), lane);
+  }
+  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
   const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
 #pragma unroll
   for (int k = 0; k < 10; k++) {
@@ -307,10 +394,11 @@ __global__ void k_check_done(const int* nsegs, const int32_t* seg_start,
 
 template <bool CLOSEST, bool LIVE>
 static void dispatch_consult(int stack, int grid, cudaStream_t st, const ConsultArgs& a) {
+  const int sl = g_consult_short;
   switch (stack) {
-    case 64: k_consult<CLOSEST, LIVE, 64><<<grid, 128, 0, st>>>(a); break;
-    case 256: k_consult<CLOSEST, LIVE, 256><<<grid, 128, 0, st>>>(a); break;
-    default: k_consult<CLOSEST, LIVE, 512><<<grid, 128, 0, st>>>(a); break;
+    case 64: k_consult<CLOSEST, LIVE, 64><<<grid, 128, 0, st>>>(a, sl); break;
+    case 256: k_consult<CLOSEST, LIVE, 256><<<grid, 128, 0, st>>>(a, sl); break;
+    default: k_consult<CLOSEST, LIVE, 512><<<grid, 128, 0, st>>>(a, sl); break;
   }
 }
 
@@ -363,8 +451,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   if ((rc = ws.get("k_cursor", n, &a.seg_cursor))) return rc;
   if ((rc = ws.get("k_app", n, &a.app))) return rc;
   if ((rc = ws.get("k_appray", n, &a.app_ray))) return rc;
-  if ((rc = ws.get("k_work", 1, &a.work))) return rc;
-  const int grid = num_sms() * 8;
+  const int grid = (int)((n + 127) / 128);  // thread t owns segment t (nsegs <= n)
   if (!c.live) {
     a.f_found = c.base_found;
     a.f_t = c.base_t;
@@ -374,7 +461,6 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.log_eval_box = c.log_eval_box;
     a.log_pred_t = c.log_pred_t;
     a.log_pred_slot = c.log_pred_slot;
-    HRPP_CK(cudaMemsetAsync(a.work, 0, sizeof(int), st));
     launch_consult(t.closest, false, b.stack, grid, st, a);
     HRPP_LAUNCHED();
   } else {
@@ -398,6 +484,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     if ((rc = ws.get("v_sapplied", n, &a.s_applied))) return rc;
     if ((rc = ws.get("v_queue", n, &a.queue))) return rc;
     if ((rc = ws.get("v_qcount", 1, &a.qcount))) return rc;
+    if ((rc = ws.get("v_need", n, &a.need))) return rc;
     a.f_found = f_found;
     a.f_t = f_t;
     a.f_slot = f_slot;
@@ -426,11 +513,13 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;
     for (int r = 0; r <= rounds + 1; r++) {
       a.spec = r == rounds ? 2 : 0;
-      HRPP_CK(cudaMemsetAsync(a.work, 0, sizeof(int), st));
-      HRPP_CK(cudaMemsetAsync(a.qcount, 0, sizeof(int), st));
+      HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
       launch_consult(t.closest, true, b.stack, grid, st, a);
       HRPP_LAUNCHED();
       if (r <= rounds) {
+        // the rays whose full traversal is needed next, compacted in ray order
+        // (coherent neighbouring rays share warps in the traversal kernel)
+        if ((rc = compact_flags(ws, a.need, n, a.queue, a.qcount, st))) return rc;
         if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, a.queue, a.qcount,
                                to, err, st)))
           return rc;

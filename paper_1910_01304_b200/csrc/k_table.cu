@@ -69,6 +69,19 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
   return 0;
 }
 
+int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, int* count_dev,
+                  cudaStream_t st) {
+  cub::CountingInputIterator<int32_t> cnt(0);
+  size_t b = 0;
+  cub::DeviceSelect::Flagged(nullptr, b, cnt, flags, out, count_dev, (int)n, st);
+  void* tmp;
+  int rc;
+  if ((rc = ws.get_raw("cf_tmp", b, &tmp))) return rc;
+  ProfScope ps(P_GROUP, st);
+  HRPP_CK(cub::DeviceSelect::Flagged(tmp, b, cnt, flags, out, count_dev, (int)n, st));
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // index maintenance
 // ---------------------------------------------------------------------------

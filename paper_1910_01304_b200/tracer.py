@@ -61,6 +61,11 @@ def set_live_rounds(rounds: int):
     _lib.check(_lib.lib.hrpp_set_live_rounds(int(rounds)), "set_live_rounds")
 
 
+def set_consult_short(length: int):
+    """Key segments with <= length rays are replayed per lane (speed only)."""
+    _lib.check(_lib.lib.hrpp_set_consult_short(int(length)), "set_consult_short")
+
+
 def trace_wave(bvh: Bvh, table: Optional[PredictorTable], mode: RenderMode, O, D, tmins,
                tmaxs, closest: bool, stats: Optional[np.ndarray] = None,
                capture_outcomes: bool = False, want_keys: bool = False, outputs=None,

@@ -458,3 +458,25 @@ def test_deferred_commit_equals_direct_and_two_block_merge(hb):
         t.record_batch(mk, mn)
     assert list(tabs[0].dump_lines()) == list(tabs[1].dump_lines())
     assert tabs[0].entry_count == ta.entry_count  # table_entries is order-independent
+
+
+@pytest.mark.parametrize("short", [0, 1, 8, 100000])
+@pytest.mark.parametrize("mode", ["limit", "live"])
+def test_consult_paths_identical(hb, short, mode):
+    """Lane-per-segment and warp-per-segment replays give the same answers."""
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden(f"wave_{mode}_p3_g0.npz")
+    b = gbvh(hb, "spheres")
+    hb.set_consult_short(short)
+    try:
+        t = hb.PredictorTable(hb.HashConfig(3), 0)
+        stats = hb.RayKindStats()
+        out = hb._trace_wave(b, t, None, hb.RenderMode(mode), inp["primary_O"], inp["primary_D"],
+                             inp["primary_tmin"], inp["primary_tmax"], stats, closest=True,
+                             log_lists=None)
+        assert np.array_equal(stats.as_array(), ref["primary_stats"])
+        for k in ("found", "t", "slot", "leaf"):
+            assert np.array_equal(out[k], ref[f"primary_{k}"]), k
+        assert list(t.dump_lines()) == list(ref["primary_dump"])
+    finally:
+        hb.set_consult_short(8)
