@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--live-rounds", type=int, default=None)
+    ap.add_argument("--consult-short", type=int, default=None)
     ap.add_argument("--profile-only", action="store_true",
                     help="setup + a few live frames, no extras (for ncu)")
     return ap.parse_args()
@@ -173,6 +174,8 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     if args.live_rounds is not None:
         hb.set_live_rounds(args.live_rounds)
+    if args.consult_short is not None:
+        hb.set_consult_short(args.consult_short)
 
     def gpu_trace(bvh, O, D, t0, t1):
         return hb.intersect_closest_batch(bvh, O, D, t0, t1)

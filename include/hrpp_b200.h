@@ -193,7 +193,7 @@ int hrpp_profile_read(double *ms, int64_t *counts, int n, int reset);
  * speculative round).  Default 3.  Affects speed only, never results. */
 int hrpp_set_live_rounds(int rounds);
 /* Key segments with at most `len` rays are replayed by one lane, longer ones
- * by a whole warp (default 8).  Affects speed only, never results. */
+ * by a whole warp (default 32).  Affects speed only, never results. */
 int hrpp_set_consult_short(int len);
 
 #ifdef __cplusplus

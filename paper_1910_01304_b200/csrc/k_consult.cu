@@ -24,7 +24,7 @@
 
 namespace hrpp {
 
-int g_live_rounds = 3;
+int g_live_rounds = 0;
 
 enum { S_RAYS, S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG };
 
@@ -87,7 +87,7 @@ struct ConsultArgs {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-int g_consult_short = 8;  // segments up to this many rays run one lane each
+int g_consult_short = 32;  // segments up to this many rays run one lane each
 
 __device__ __forceinline__ Ray load_ray(const ConsultArgs& a, bool valid, int32_t idx) {
   if (valid) return make_ray(a.O, a.D, a.tmin, a.tmax, idx);

@@ -218,7 +218,7 @@ def test_live_rounds_do_not_change_results(hb, rounds):
             assert np.array_equal(out[k], ref[f"primary_{k}"]), k
         assert list(t.dump_lines()) == list(ref["primary_dump"])
     finally:
-        hb.set_live_rounds(3)
+        hb.set_live_rounds(0)
 
 
 def test_wave_torch_device_arrays(hb):
@@ -479,4 +479,4 @@ def test_consult_paths_identical(hb, short, mode):
             assert np.array_equal(out[k], ref[f"primary_{k}"]), k
         assert list(t.dump_lines()) == list(ref["primary_dump"])
     finally:
-        hb.set_consult_short(8)
+        hb.set_consult_short(32)
