@@ -130,6 +130,7 @@ struct Segments {
   int32_t* sidx = nullptr;
   int32_t* seg_start = nullptr;  // nsegs + 1 entries (device count)
   int* nsegs = nullptr;          // device scalar
+  int32_t* seg_id = nullptr;     // per sorted position: segment index + 1
 };
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
                  cudaStream_t st);

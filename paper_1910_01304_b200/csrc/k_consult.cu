@@ -3,30 +3,46 @@
 // The reference consults and trains the table one ray at a time in wave
 // order (hrpp/tracer.py:233-267 limit, :295-331 live).  A table entry is
 // read and written only by rays carrying its key, so the loop is
-// independent per key: after a stable sort by key, one warp replays each
-// key segment in ray order.  Lanes hold 32 consecutive rays of the segment;
-// each lane folds the entry's nodes into its running eval_entry result
-// (hrpp/kernels.py:251-297) incrementally, so a node appended by ray f is
-// evaluated only by the rays after f -- exactly the (ray, node) pairs the
-// sequential loop evaluates.  A ballot finds the next ray that is not a
-// true positive; the rays before it commit as TPs, it commits as NEG/FP
-// and may append anc[leaf] (de-duplicated) to the entry.
+// independent per key; after a stable sort by key the wave is a set of key
+// segments, each replayed in ray order.  The work splits in two:
 //
-// Live mode needs the full-traversal result of every non-TP ray, which the
-// reference computes inline.  Here the warp suspends at the first such ray
-// whose result is unknown and enqueues it; a dense traversal kernel traces
-// the queue; the consult resumes.  After `g_live_rounds` exact rounds one
-// speculative round enqueues every ray of the remaining segments that is
-// not yet a TP (TP status is monotone in entry growth, so every ray that can
-// still need a full result is then traced) and a final round completes all
-// segments.  Speculation only costs extra traversals; results are exact.
+//  1. k_eval0 -- ray-parallel, one thread per sorted position: evaluate the
+//     entry as it stood at the start of the wave (hrpp/kernels.py:251-297)
+//     for every ray.  A ray that hits here is a true positive whatever the
+//     wave appends later (entries only grow and every node is evaluated).
+//  2. k_replay -- per key segment, in ray order: fold the nodes appended
+//     earlier in this wave into each ray's running result, classify
+//     TP / FP / NEG, and append anc[leaf] (de-duplicated) after each non-TP
+//     ray with a hit.  Short segments run one lane each, long ones on a
+//     whole warp whose lanes hold 32 consecutive rays (a ballot finds the
+//     next non-TP ray).
+//
+// Limit mode knows every full-traversal result up front.  Live mode needs
+// the full result of each non-TP ray: by default (g_live_rounds = 0) every
+// ray that is not a TP against the wave-start entry is traced (one dense,
+// ray-ordered traversal launch) before a single replay.  With rounds > 0 the
+// replay suspends at the first ray of a segment whose full result is
+// unknown, the queue is traced and the replay resumes; after `rounds` exact
+// rounds one speculative round traces every unresolved ray.  Either way the
+// results are exact: speculation only costs traversals.
 #include "hrpp_internal.h"
 
 namespace hrpp {
 
 int g_live_rounds = 0;
+int g_consult_short = 32;  // segments up to this many rays are replayed by one lane
 
 enum { S_RAYS, S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG };
+
+// Running eval_entry result of one ray (by sorted position): 32 bytes, two
+// 16-B accesses.  `applied` = number of entry nodes already folded.
+struct __align__(16) RayState {
+  double t;
+  int32_t slot, leaf;
+  int32_t boxes, tris;
+  int32_t applied;
+  int32_t found;
+};
 
 struct ConsultArgs {
   const DNode* nodes;
@@ -40,6 +56,7 @@ struct ConsultArgs {
   const unsigned long long* skeys;
   const int32_t* sidx;
   const int32_t* seg_start;
+  const int32_t* seg_id;
   const int* nsegs;
   const unsigned long long* idx_keys;
   const int32_t* idx_vals;
@@ -47,11 +64,15 @@ struct ConsultArgs {
   const int64_t* e_off;
   const int32_t* e_len;
   const int32_t* arena;
+  // per segment
   int32_t* seg_eid;
+  int64_t* seg_exoff;
+  int32_t* seg_exlen;
   int32_t* seg_napp;
   int32_t* seg_cursor;
-  int32_t* app;
+  int32_t* app;      // appended nodes of segment s live at app[seg_start[s] ...]
   int32_t* app_ray;  // ray index that triggered each append (deferred mode)
+  RayState* state;   // per sorted position
   // full-traversal results by ray index (baseline in limit mode)
   const uint8_t* f_found;
   const double* f_t;
@@ -59,15 +80,7 @@ struct ConsultArgs {
   const int32_t* f_leaf;
   const int64_t* f_box;
   const int64_t* f_tri;
-  const uint8_t* f_known;
-  // live per-ray consult state by sorted position
-  uint8_t* s_found;
-  double* s_t;
-  int32_t* s_slot;
-  int32_t* s_leaf;
-  int32_t* s_box;
-  int32_t* s_tri;
-  int32_t* s_applied;
+  const uint8_t* f_known;  // live only
   // outputs by ray index
   uint8_t* o_found;
   double* o_t;
@@ -78,45 +91,38 @@ struct ConsultArgs {
   double* log_pred_t;
   int64_t* log_pred_slot;
   unsigned long long* stats;
-  uint8_t* need;  // live: rays whose full traversal the consult needs next
-  int32_t* queue;
-  int* qcount;
-  int spec;  // 0: enqueue the first unknown ray; 2: enqueue every unresolved ray
+  uint8_t* need;  // live: rays whose full traversal is needed next
+  int spec;       // live replay: 0 mark the first unknown ray, 2 mark every unresolved ray
   const int* err;
 };
 
 constexpr unsigned kFull = 0xffffffffu;
 
-int g_consult_short = 32;  // segments up to this many rays run one lane each
-
-__device__ __forceinline__ Ray load_ray(const ConsultArgs& a, bool valid, int32_t idx) {
-  if (valid) return make_ray(a.O, a.D, a.tmin, a.tmax, idx);
-  Ray r{};
-  return r;
-}
-
 __device__ __forceinline__ void load_state(const ConsultArgs& a, int32_t pos, Hit& acc,
                                            int32_t& applied) {
-  applied = a.s_applied[pos];
-  if (applied > 0) {
-    acc.found = a.s_found[pos];
-    acc.t = a.s_t[pos];
-    acc.slot = a.s_slot[pos];
-    acc.leaf = a.s_leaf[pos];
-    acc.boxes = a.s_box[pos];
-    acc.tris = a.s_tri[pos];
-  }
+  const RayState s = a.state[pos];
+  acc.found = s.found != 0;
+  acc.t = s.t;
+  acc.slot = s.slot;
+  acc.leaf = s.leaf;
+  acc.u = 0.0;
+  acc.v = 0.0;
+  acc.boxes = s.boxes;
+  acc.tris = s.tris;
+  applied = s.applied;
 }
 
 __device__ __forceinline__ void store_state(const ConsultArgs& a, int32_t pos, const Hit& acc,
                                             int32_t applied) {
-  a.s_applied[pos] = applied;
-  a.s_found[pos] = acc.found;
-  a.s_t[pos] = acc.t;
-  a.s_slot[pos] = acc.slot;
-  a.s_leaf[pos] = acc.leaf;
-  a.s_box[pos] = acc.boxes;
-  a.s_tri[pos] = acc.tris;
+  RayState s;
+  s.t = acc.t;
+  s.slot = acc.slot;
+  s.leaf = acc.leaf;
+  s.boxes = acc.boxes;
+  s.tris = acc.tris;
+  s.applied = applied;
+  s.found = acc.found;
+  a.state[pos] = s;
 }
 
 struct Tally {
@@ -189,6 +195,45 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
   }
 }
 
+// ---------------------------------------------------------------------------
+// stage 1: per segment entry lookup, then per ray wave-start evaluation
+// ---------------------------------------------------------------------------
+
+__global__ void k_seg_lookup(ConsultArgs a, int64_t n) {
+  const int ns = *a.nsegs;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t beg = a.seg_start[s];
+    const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
+    a.seg_eid[s] = eid;
+    a.seg_exoff[s] = eid >= 0 ? a.e_off[eid] : 0;
+    a.seg_exlen[s] = eid >= 0 ? a.e_len[eid] : 0;
+    a.seg_napp[s] = 0;
+    a.seg_cursor[s] = beg;
+  }
+}
+
+template <bool CLOSEST, int STACK>
+__global__ void __launch_bounds__(128) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
+  if (*a.err) return;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = a.seg_id[p] - 1;
+    const int32_t ex_len = a.seg_exlen[s];
+    Hit acc = empty_entry_result(CLOSEST);
+    if (ex_len > 0) {
+      const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, a.sidx[p]);
+      catch_up<CLOSEST, STACK>(a, r, acc, 0, ex_len, a.seg_exoff[s], ex_len, nullptr);
+    }
+    store_state(a, (int32_t)p, acc, ex_len);
+    if (mark_need && !(ex_len > 0 && acc.found)) a.need[a.sidx[p]] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stage 2: per segment replay in ray order
+// ---------------------------------------------------------------------------
+
 // Speculative round: every not-yet-TP ray of the rest of the segment gets its
 // full traversal (TP status only grows with the entry, so after this round
 // every ray that can still need a full result has one).
@@ -197,35 +242,37 @@ __device__ void speculate_rest(const ConsultArgs& a, int32_t from, int32_t end, 
                                int64_t ex_off, int32_t ex_len, const int32_t* app) {
   for (int32_t j = from; j < end; j++) {
     const int32_t idx = a.sidx[j];
-    const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
-    Hit acc = empty_entry_result(CLOSEST);
-    int32_t applied = 0;
+    Hit acc;
+    int32_t applied;
     load_state(a, j, acc, applied);
-    catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
-    store_state(a, j, acc, L);
+    if (applied < L && (CLOSEST || !acc.found)) {
+      const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+      catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+      store_state(a, j, acc, L);
+    }
     if (!(L > 0 && acc.found) && !a.f_known[idx]) a.need[idx] = 1;
   }
 }
 
-// One short key segment, replayed by one lane (hrpp/tracer.py:233-267 or
-// :295-331 restricted to one key).
+// One short key segment, replayed by one lane.
 template <bool CLOSEST, bool LIVE, int STACK>
 __device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, int32_t end,
                            int32_t cur) {
-  const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
-  const int64_t ex_off = eid >= 0 ? a.e_off[eid] : 0;
-  const int32_t ex_len = eid >= 0 ? a.e_len[eid] : 0;
+  const int64_t ex_off = a.seg_exoff[s];
+  const int32_t ex_len = a.seg_exlen[s];
   int32_t* app = a.app + beg;
-  int32_t napp = LIVE ? a.seg_napp[s] : 0;
+  int32_t napp = a.seg_napp[s];
   int32_t j = cur;
   for (; j < end; j++) {
     const int32_t idx = a.sidx[j];
-    const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
-    Hit acc = empty_entry_result(CLOSEST);
-    int32_t applied = 0;
-    if (LIVE) load_state(a, j, acc, applied);
+    Hit acc;
+    int32_t applied;
+    load_state(a, j, acc, applied);
     const int32_t L = ex_len + napp;
-    catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+    if (applied < L && (CLOSEST || !acc.found)) {
+      const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+      catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+    }
     if (L > 0 && acc.found) {
       commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
       continue;
@@ -248,9 +295,8 @@ __device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, i
       }
     }
   }
-  if (LIVE) a.seg_cursor[s] = j;
+  a.seg_cursor[s] = j;
   a.seg_napp[s] = napp;
-  a.seg_eid[s] = eid;
 }
 
 // One long key segment, replayed by the whole warp: lanes hold 32
@@ -258,28 +304,29 @@ __device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, i
 template <bool CLOSEST, bool LIVE, int STACK>
 __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
   const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
-  int32_t tb = LIVE ? a.seg_cursor[s] : beg;
-  int32_t napp = LIVE ? a.seg_napp[s] : 0;
-  const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
-  const int64_t ex_off = eid >= 0 ? a.e_off[eid] : 0;
-  const int32_t ex_len = eid >= 0 ? a.e_len[eid] : 0;
+  int32_t tb = a.seg_cursor[s];
+  int32_t napp = a.seg_napp[s];
+  const int64_t ex_off = a.seg_exoff[s];
+  const int32_t ex_len = a.seg_exlen[s];
   int32_t* app = a.app + beg;
   bool suspended = false;
   while (tb < end) {
     const int32_t pos = tb + lane;
     const bool valid = pos < end;
     const int32_t idx = valid ? a.sidx[pos] : 0;
-    const Ray r = load_ray(a, valid, idx);
     Hit acc = empty_entry_result(CLOSEST);
     int32_t applied = 0;
-    if (LIVE && valid) load_state(a, pos, acc, applied);
+    if (valid) load_state(a, pos, acc, applied);
     int32_t L = ex_len + napp;
     const bool fknown = valid && (!LIVE || a.f_known[idx]);
     int32_t cnode = -1;
     if (fknown && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
     bool inL = false;
     for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
-    if (valid) catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+    Ray r{};
+    if (valid) r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+    if (valid && applied < L && (CLOSEST || !acc.found))
+      catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
     applied = L;
     int cursor = 0;
     for (;;) {
@@ -294,12 +341,14 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
         if (a.spec >= 2) {
           for (int32_t t2 = tb + 32 + lane; t2 < end; t2 += 32) {
             const int32_t i2 = a.sidx[t2];
-            const Ray r2 = make_ray(a.O, a.D, a.tmin, a.tmax, i2);
-            Hit a2 = empty_entry_result(CLOSEST);
-            int32_t ap2 = 0;
+            Hit a2;
+            int32_t ap2;
             load_state(a, t2, a2, ap2);
-            catch_up<CLOSEST, STACK>(a, r2, a2, ap2, L, ex_off, ex_len, app);
-            store_state(a, t2, a2, L);
+            if (ap2 < L && (CLOSEST || !a2.found)) {
+              const Ray r2 = make_ray(a.O, a.D, a.tmin, a.tmax, i2);
+              catch_up<CLOSEST, STACK>(a, r2, a2, ap2, L, ex_off, ex_len, app);
+              store_state(a, t2, a2, L);
+            }
             if (!(L > 0 && a2.found) && !a.f_known[i2]) a.need[i2] = 1;
           }
         }
@@ -323,7 +372,8 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
         napp++;
         L++;
         inL |= cnode == cf;
-        if (valid && lane > f) catch_up<CLOSEST, STACK>(a, r, acc, L - 1, L, ex_off, ex_len, app);
+        if (valid && lane > f && (CLOSEST || !acc.found))
+          catch_up<CLOSEST, STACK>(a, r, acc, L - 1, L, ex_off, ex_len, app);
         applied = L;
       }
       cursor = f + 1;
@@ -331,19 +381,16 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
     if (suspended) break;
     tb += 32;
   }
-  if (lane == 0) {
-    a.seg_eid[s] = eid;
-    if (!suspended) {
-      a.seg_napp[s] = napp;
-      if (LIVE) a.seg_cursor[s] = end;
-    }
+  if (lane == 0 && !suspended) {
+    a.seg_napp[s] = napp;
+    a.seg_cursor[s] = end;
   }
 }
 
 // Thread t owns key segment t; segments longer than `short_len` rays are
-// replayed cooperatively by the owning warp.  No global work queue.
+// replayed cooperatively by the owning warp.
 template <bool CLOSEST, bool LIVE, int STACK>
-__global__ void __launch_bounds__(128) k_consult(ConsultArgs a, int short_len) {
+__global__ void __launch_bounds__(128) k_replay(ConsultArgs a, int short_len) {
   if (*a.err) return;
   const int lane = threadIdx.x & 31;
   const int ns = *a.nsegs;
@@ -354,7 +401,7 @@ __global__ void __launch_bounds__(128) k_consult(ConsultArgs a, int short_len) {
   if (s < ns) {
     beg = a.seg_start[s];
     end = a.seg_start[s + 1];
-    cur = LIVE ? a.seg_cursor[s] : beg;
+    cur = a.seg_cursor[s];
     active = cur < end;
     small = end - beg <= short_len;
   }
@@ -374,17 +421,6 @@ __global__ void __launch_bounds__(128) k_consult(ConsultArgs a, int short_len) {
   }
 }
 
-__global__ void k_seg_init(const int* nsegs, const int32_t* seg_start, int32_t* seg_cursor,
-                           int32_t* seg_napp, int32_t* seg_eid, int64_t n) {
-  const int ns = *nsegs;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    seg_cursor[s] = seg_start[s];
-    seg_napp[s] = 0;
-    seg_eid[s] = -1;
-  }
-}
-
 __global__ void k_check_done(const int* nsegs, const int32_t* seg_start,
                              const int32_t* seg_cursor, int* err) {
   const int ns = *nsegs;
@@ -392,25 +428,39 @@ __global__ void k_check_done(const int* nsegs, const int32_t* seg_start,
     if (seg_cursor[s] < seg_start[s + 1]) atomicCAS(err, 0, 4);
 }
 
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
 template <bool CLOSEST, bool LIVE>
-static void dispatch_consult(int stack, int grid, cudaStream_t st, const ConsultArgs& a) {
+static void dispatch_replay(int stack, int grid, cudaStream_t st, const ConsultArgs& a) {
   const int sl = g_consult_short;
   switch (stack) {
-    case 64: k_consult<CLOSEST, LIVE, 64><<<grid, 128, 0, st>>>(a, sl); break;
-    case 256: k_consult<CLOSEST, LIVE, 256><<<grid, 128, 0, st>>>(a, sl); break;
-    default: k_consult<CLOSEST, LIVE, 512><<<grid, 128, 0, st>>>(a, sl); break;
+    case 64: k_replay<CLOSEST, LIVE, 64><<<grid, 128, 0, st>>>(a, sl); break;
+    case 256: k_replay<CLOSEST, LIVE, 256><<<grid, 128, 0, st>>>(a, sl); break;
+    default: k_replay<CLOSEST, LIVE, 512><<<grid, 128, 0, st>>>(a, sl); break;
   }
 }
 
-static void launch_consult(bool closest, bool live, int stack, int grid, cudaStream_t st,
-                           const ConsultArgs& a) {
+static void launch_replay(bool closest, bool live, int stack, int grid, cudaStream_t st,
+                          const ConsultArgs& a) {
   ProfScope ps(P_CONSULT, st);
   if (closest) {
-    if (live) dispatch_consult<true, true>(stack, grid, st, a);
-    else dispatch_consult<true, false>(stack, grid, st, a);
+    if (live) dispatch_replay<true, true>(stack, grid, st, a);
+    else dispatch_replay<true, false>(stack, grid, st, a);
   } else {
-    if (live) dispatch_consult<false, true>(stack, grid, st, a);
-    else dispatch_consult<false, false>(stack, grid, st, a);
+    if (live) dispatch_replay<false, true>(stack, grid, st, a);
+    else dispatch_replay<false, false>(stack, grid, st, a);
+  }
+}
+
+template <bool CLOSEST>
+static void dispatch_eval0(int stack, int grid, cudaStream_t st, const ConsultArgs& a, int64_t n,
+                           int mark) {
+  switch (stack) {
+    case 64: k_eval0<CLOSEST, 64><<<grid, 128, 0, st>>>(a, n, mark); break;
+    case 256: k_eval0<CLOSEST, 256><<<grid, 128, 0, st>>>(a, n, mark); break;
+    default: k_eval0<CLOSEST, 512><<<grid, 128, 0, st>>>(a, n, mark); break;
   }
 }
 
@@ -437,6 +487,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   a.skeys = seg.skeys;
   a.sidx = seg.sidx;
   a.seg_start = seg.seg_start;
+  a.seg_id = seg.seg_id;
   a.nsegs = seg.nsegs;
   a.idx_keys = t.idx_keys;
   a.idx_vals = t.idx_vals;
@@ -446,45 +497,30 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   a.arena = t.arena;
   a.stats = stats_dev;
   a.err = err;
-  if ((rc = ws.get("k_eid", n, &a.seg_eid))) return rc;
-  if ((rc = ws.get("k_napp", n, &a.seg_napp))) return rc;
-  if ((rc = ws.get("k_cursor", n, &a.seg_cursor))) return rc;
-  if ((rc = ws.get("k_app", n, &a.app))) return rc;
-  if ((rc = ws.get("k_appray", n, &a.app_ray))) return rc;
+  if ((rc = ws.get("k_eid", n, &a.seg_eid)) || (rc = ws.get("k_exoff", n, &a.seg_exoff)) ||
+      (rc = ws.get("k_exlen", n, &a.seg_exlen)) || (rc = ws.get("k_napp", n, &a.seg_napp)) ||
+      (rc = ws.get("k_cursor", n, &a.seg_cursor)) || (rc = ws.get("k_app", n, &a.app)) ||
+      (rc = ws.get("k_appray", n, &a.app_ray)) || (rc = ws.get("k_state", n, &a.state)))
+    return rc;
   const int grid = (int)((n + 127) / 128);  // thread t owns segment t (nsegs <= n)
-  if (!c.live) {
-    a.f_found = c.base_found;
-    a.f_t = c.base_t;
-    a.f_leaf = c.base_leaf;
-    a.f_box = c.base_box;
-    a.log_cls = c.log_cls;
-    a.log_eval_box = c.log_eval_box;
-    a.log_pred_t = c.log_pred_t;
-    a.log_pred_slot = c.log_pred_slot;
-    launch_consult(t.closest, false, b.stack, grid, st, a);
+  {
+    ProfScope ps(P_CONSULT, st);
+    k_seg_lookup<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a, n);
     HRPP_LAUNCHED();
-  } else {
+  }
+  const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;
+  if (c.live) {
     uint8_t *f_found, *f_known;
     double* f_t;
-    int32_t *f_slot, *f_leaf;
+    int32_t *f_slot, *f_leaf, *queue;
     int64_t *f_box, *f_tri;
-    if ((rc = ws.get("v_ffound", n, &f_found))) return rc;
-    if ((rc = ws.get("v_fknown", n, &f_known))) return rc;
-    if ((rc = ws.get("v_ft", n, &f_t))) return rc;
-    if ((rc = ws.get("v_fslot", n, &f_slot))) return rc;
-    if ((rc = ws.get("v_fleaf", n, &f_leaf))) return rc;
-    if ((rc = ws.get("v_fbox", n, &f_box))) return rc;
-    if ((rc = ws.get("v_ftri", n, &f_tri))) return rc;
-    if ((rc = ws.get("v_sfound", n, &a.s_found))) return rc;
-    if ((rc = ws.get("v_st", n, &a.s_t))) return rc;
-    if ((rc = ws.get("v_sslot", n, &a.s_slot))) return rc;
-    if ((rc = ws.get("v_sleaf", n, &a.s_leaf))) return rc;
-    if ((rc = ws.get("v_sbox", n, &a.s_box))) return rc;
-    if ((rc = ws.get("v_stri", n, &a.s_tri))) return rc;
-    if ((rc = ws.get("v_sapplied", n, &a.s_applied))) return rc;
-    if ((rc = ws.get("v_queue", n, &a.queue))) return rc;
-    if ((rc = ws.get("v_qcount", 1, &a.qcount))) return rc;
-    if ((rc = ws.get("v_need", n, &a.need))) return rc;
+    int* qcount;
+    if ((rc = ws.get("v_ffound", n, &f_found)) || (rc = ws.get("v_fknown", n, &f_known)) ||
+        (rc = ws.get("v_ft", n, &f_t)) || (rc = ws.get("v_fslot", n, &f_slot)) ||
+        (rc = ws.get("v_fleaf", n, &f_leaf)) || (rc = ws.get("v_fbox", n, &f_box)) ||
+        (rc = ws.get("v_ftri", n, &f_tri)) || (rc = ws.get("v_queue", n, &queue)) ||
+        (rc = ws.get("v_qcount", 1, &qcount)) || (rc = ws.get("v_need", n, &a.need)))
+      return rc;
     a.f_found = f_found;
     a.f_t = f_t;
     a.f_slot = f_slot;
@@ -497,11 +533,13 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.o_slot = c.o_slot;
     a.o_leaf = c.o_leaf;
     HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
-    HRPP_CK(cudaMemsetAsync(a.s_applied, 0, sizeof(int32_t) * n, st));
-    k_seg_init<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(seg.nsegs, seg.seg_start,
-                                                               a.seg_cursor, a.seg_napp,
-                                                               a.seg_eid, n);
-    HRPP_LAUNCHED();
+    HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
+    {
+      ProfScope ps(P_CONSULT, st);
+      if (t.closest) dispatch_eval0<true>(b.stack, grid, st, a, n, rounds == 0);
+      else dispatch_eval0<false>(b.stack, grid, st, a, n, rounds == 0);
+      HRPP_LAUNCHED();
+    }
     TraceOut to;
     to.found = f_found;
     to.t = f_t;
@@ -510,23 +548,45 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     to.box = f_box;
     to.tri = f_tri;
     to.known = f_known;
-    const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;
-    for (int r = 0; r <= rounds + 1; r++) {
-      a.spec = r == rounds ? 2 : 0;
-      HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
-      launch_consult(t.closest, true, b.stack, grid, st, a);
-      HRPP_LAUNCHED();
-      if (r <= rounds) {
-        // the rays whose full traversal is needed next, compacted in ray order
-        // (coherent neighbouring rays share warps in the traversal kernel)
-        if ((rc = compact_flags(ws, a.need, n, a.queue, a.qcount, st))) return rc;
-        if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, a.queue, a.qcount,
-                               to, err, st)))
-          return rc;
+    // rounds == 0: eval0 already marked every ray that is not a TP against the
+    // wave-start entry; trace them, then one replay completes the wave.
+    // rounds > 0: exact replay rounds, the last one speculative.
+    for (int r = rounds == 0 ? rounds : 0; r <= rounds; r++) {
+      if (rounds > 0) {
+        a.spec = r == rounds ? 2 : 0;
+        HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
+        launch_replay(t.closest, true, b.stack, grid, st, a);
+        HRPP_LAUNCHED();
       }
+      // the rays whose full traversal is needed next, compacted in ray order
+      // (coherent neighbouring rays share warps in the traversal kernel)
+      if ((rc = compact_flags(ws, a.need, n, queue, qcount, st))) return rc;
+      if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, queue, qcount, to,
+                             err, st)))
+        return rc;
     }
+    a.spec = 0;
+    launch_replay(t.closest, true, b.stack, grid, st, a);
+    HRPP_LAUNCHED();
     k_check_done<<<grid_for(n, 256, num_sms() * 4), 256, 0, st>>>(seg.nsegs, seg.seg_start,
                                                                  a.seg_cursor, err);
+    HRPP_LAUNCHED();
+  } else {
+    a.f_found = c.base_found;
+    a.f_t = c.base_t;
+    a.f_leaf = c.base_leaf;
+    a.f_box = c.base_box;
+    a.log_cls = c.log_cls;
+    a.log_eval_box = c.log_eval_box;
+    a.log_pred_t = c.log_pred_t;
+    a.log_pred_slot = c.log_pred_slot;
+    {
+      ProfScope ps(P_CONSULT, st);
+      if (t.closest) dispatch_eval0<true>(b.stack, grid, st, a, n, 0);
+      else dispatch_eval0<false>(b.stack, grid, st, a, n, 0);
+      HRPP_LAUNCHED();
+    }
+    launch_replay(t.closest, false, b.stack, grid, st, a);
     HRPP_LAUNCHED();
   }
   if (t.deferred)

@@ -24,7 +24,7 @@ __global__ void k_iota(int32_t* v, int64_t n) {
 }
 
 __global__ void k_head_flags(const unsigned long long* __restrict__ sk, int64_t n,
-                             uint8_t* __restrict__ flags) {
+                             int32_t* __restrict__ flags) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     flags[i] = (i == 0) || (sk[i] != sk[i - 1]);
@@ -37,7 +37,7 @@ __global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n) 
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
                  cudaStream_t st) {
   int32_t* iota;
-  uint8_t* flags;
+  int32_t* flags;
   int rc;
   if ((rc = ws.get("g_skeys", n, &seg->skeys))) return rc;
   if ((rc = ws.get("g_iota", n, &iota))) return rc;
@@ -45,25 +45,31 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
   if ((rc = ws.get("g_flags", n, &flags))) return rc;
   if ((rc = ws.get("g_segstart", n + 1, &seg->seg_start))) return rc;
   if ((rc = ws.get("g_nsegs", 1, &seg->nsegs))) return rc;
+  if ((rc = ws.get("g_segid", n, &seg->seg_id))) return rc;
   int grid = grid_for(n, 256, num_sms() * 8);
   ProfScope ps(P_GROUP, st);
   k_iota<<<grid, 256, 0, st>>>(iota, n);
   HRPP_LAUNCHED();
   const unsigned long long* kin = reinterpret_cast<const unsigned long long*>(keys);
-  size_t b_sort = 0, b_sel = 0;
+  size_t b_sort = 0, b_sel = 0, b_scan = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, b_sort, kin, seg->skeys, iota, seg->sidx, (int)n,
                                   0, 48, st);
   cub::CountingInputIterator<int32_t> cnt(0);
   cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
                              st);
+  cub::DeviceScan::InclusiveSum(nullptr, b_scan, flags, seg->seg_id, (int)n, st);
+  size_t b = b_sort > b_sel ? b_sort : b_sel;
+  b = b > b_scan ? b : b_scan;
   void* tmp;
-  if ((rc = ws.get_raw("g_cubtmp", b_sort > b_sel ? b_sort : b_sel, &tmp))) return rc;
+  if ((rc = ws.get_raw("g_cubtmp", b, &tmp))) return rc;
   HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b_sort, kin, seg->skeys, iota, seg->sidx, (int)n,
                                           0, 48, st));
   k_head_flags<<<grid, 256, 0, st>>>(seg->skeys, n, flags);
   HRPP_LAUNCHED();
   HRPP_CK(cub::DeviceSelect::Flagged(tmp, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
                                      st));
+  // seg_id[p] = 1 + index of the key segment holding sorted position p
+  HRPP_CK(cub::DeviceScan::InclusiveSum(tmp, b_scan, flags, seg->seg_id, (int)n, st));
   k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n);
   HRPP_LAUNCHED();
   return 0;
