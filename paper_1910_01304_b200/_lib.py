@@ -14,7 +14,10 @@ import numpy as np
 
 from .errors import CapacityExceeded, NonFiniteInput
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhrpp_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("HRPP_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libhrpp_b200.so")
 
 OK, NONFINITE, CAPACITY, INVALID_ARG, CUDA_ERR = 0, 1, 2, 3, 4
 HIT_ANY, CLOSEST_HIT = 0, 1

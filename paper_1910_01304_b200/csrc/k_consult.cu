@@ -91,7 +91,8 @@ struct ConsultArgs {
   double* log_pred_t;
   int64_t* log_pred_slot;
   unsigned long long* stats;
-  uint8_t* need;  // live: rays whose full traversal is needed next
+  uint8_t* need;  // live: rays (by index) whose full traversal is needed next
+  int32_t* seg_f1;  // first sorted position of the segment that appends (or INT_MAX)
   int spec;       // live replay: 0 mark the first unknown ray, 2 mark every unresolved ray
   const int* err;
 };
@@ -210,6 +211,71 @@ __global__ void k_seg_lookup(ConsultArgs a, int64_t n) {
     a.seg_exlen[s] = eid >= 0 ? a.e_len[eid] : 0;
     a.seg_napp[s] = 0;
     a.seg_cursor[s] = beg;
+    a.seg_f1[s] = 0x7fffffff;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stage 1b (all full results known): rays up to and including the first ray
+// of their segment that appends see exactly the wave-start entry, so they
+// are classified ray-parallel; only the rest of each segment is replayed.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ bool in_list(const ConsultArgs& a, int64_t off, int32_t len,
+                                        int32_t node) {
+  for (int32_t k = 0; k < len; k++)
+    if (a.arena[off + k] == node) return true;
+  return false;
+}
+
+__global__ void k_first_append(ConsultArgs a, int64_t n) {
+  if (*a.err) return;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const RayState st = a.state[p];
+    const int32_t s = a.seg_id[p] - 1;
+    const int32_t ex_len = a.seg_exlen[s];
+    if (ex_len > 0 && st.found) continue;  // TP against the wave-start entry
+    const int32_t idx = a.sidx[p];
+    if (!a.f_found[idx]) continue;
+    if (!in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[idx]]))
+      atomicMin(a.seg_f1 + s, (int32_t)p);
+  }
+}
+
+template <bool CLOSEST, bool LIVE>
+__global__ void __launch_bounds__(128) k_finalize(ConsultArgs a, int64_t n) {
+  if (*a.err) return;
+  Tally c;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = a.seg_id[p] - 1;
+    const int32_t f1 = a.seg_f1[s];
+    const int32_t beg = a.seg_start[s];
+    if (p > f1) continue;  // after the first append: replayed
+    Hit acc;
+    int32_t applied;
+    load_state(a, (int32_t)p, acc, applied);
+    const int32_t ex_len = a.seg_exlen[s];
+    const int32_t idx = a.sidx[p];
+    if (ex_len > 0 && acc.found) commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+    else commit_miss<LIVE>(a, c, idx, acc, ex_len == 0);
+    if (p == f1) {  // the first record(key, anc[leaf]) of this segment
+      a.app[beg] = a.anc[a.f_leaf[idx]];
+      a.app_ray[beg] = idx;
+      a.seg_napp[s] = 1;
+      a.seg_cursor[s] = f1 + 1;
+    } else if (p == beg && f1 == 0x7fffffff) {
+      a.seg_cursor[s] = a.seg_start[s + 1];  // no append: the segment is done
+    }
+  }
+  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
+  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 10; k++) {
+    long long w = warp_sum(v[k]);
+    if (lane == 0 && w) atomicAdd(a.stats + slot[k], (unsigned long long)w);
   }
 }
 
@@ -464,6 +530,22 @@ static void dispatch_eval0(int stack, int grid, cudaStream_t st, const ConsultAr
   }
 }
 
+static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
+                           const ConsultArgs& a, int64_t n) {
+  ProfScope ps(P_CONSULT, st);
+  k_first_append<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
+  HRPP_LAUNCHED();
+  if (closest) {
+    if (live) k_finalize<true, true><<<grid, 128, 0, st>>>(a, n);
+    else k_finalize<true, false><<<grid, 128, 0, st>>>(a, n);
+  } else {
+    if (live) k_finalize<false, true><<<grid, 128, 0, st>>>(a, n);
+    else k_finalize<false, false><<<grid, 128, 0, st>>>(a, n);
+  }
+  HRPP_LAUNCHED();
+  return 0;
+}
+
 int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* keys,
                 unsigned long long* stats_dev, int* err, cudaStream_t st) {
   const int64_t n = c.n;
@@ -500,7 +582,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   if ((rc = ws.get("k_eid", n, &a.seg_eid)) || (rc = ws.get("k_exoff", n, &a.seg_exoff)) ||
       (rc = ws.get("k_exlen", n, &a.seg_exlen)) || (rc = ws.get("k_napp", n, &a.seg_napp)) ||
       (rc = ws.get("k_cursor", n, &a.seg_cursor)) || (rc = ws.get("k_app", n, &a.app)) ||
-      (rc = ws.get("k_appray", n, &a.app_ray)) || (rc = ws.get("k_state", n, &a.state)))
+      (rc = ws.get("k_appray", n, &a.app_ray)) || (rc = ws.get("k_state", n, &a.state)) ||
+      (rc = ws.get("k_f1", n, &a.seg_f1)))
     return rc;
   const int grid = (int)((n + 127) / 128);  // thread t owns segment t (nsegs <= n)
   {
@@ -558,14 +641,18 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
         launch_replay(t.closest, true, b.stack, grid, st, a);
         HRPP_LAUNCHED();
       }
-      // the rays whose full traversal is needed next, compacted in ray order
-      // (coherent neighbouring rays share warps in the traversal kernel)
+      // the rays whose full traversal is needed next, compacted in ray order:
+      // neighbouring pixels share warps in the traversal kernel (key order
+      // is worse: the xor-mixed key scatters unrelated rays into one warp)
       if ((rc = compact_flags(ws, a.need, n, queue, qcount, st))) return rc;
       if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, queue, qcount, to,
                              err, st)))
         return rc;
     }
     a.spec = 0;
+    if (rounds == 0) {
+      if ((rc = finalize_prefix(t.closest, true, grid, st, a, n))) return rc;
+    }
     launch_replay(t.closest, true, b.stack, grid, st, a);
     HRPP_LAUNCHED();
     k_check_done<<<grid_for(n, 256, num_sms() * 4), 256, 0, st>>>(seg.nsegs, seg.seg_start,
@@ -586,6 +673,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       else dispatch_eval0<false>(b.stack, grid, st, a, n, 0);
       HRPP_LAUNCHED();
     }
+    if ((rc = finalize_prefix(t.closest, false, grid, st, a, n))) return rc;
     launch_replay(t.closest, false, b.stack, grid, st, a);
     HRPP_LAUNCHED();
   }

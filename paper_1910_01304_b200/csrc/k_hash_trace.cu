@@ -131,10 +131,12 @@ struct TraceArgs {
 template <bool CLOSEST, int STACK>
 __global__ void __launch_bounds__(128) k_trace(TraceArgs a) {
   if (a.err && *a.err) return;
+  // one ray per thread; with a device-side count (fallback queue) the grid is
+  // sized for the host-known upper bound and surplus threads exit at once
   const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.n;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long sb = 0, stt = 0;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count;
-       q += (int64_t)gridDim.x * blockDim.x) {
+  if (q < count) {
     const int64_t i = a.ray_idx ? (int64_t)a.ray_idx[q] : q;
     Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
     Hit h = trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, a.start);
@@ -149,8 +151,8 @@ __global__ void __launch_bounds__(128) k_trace(TraceArgs a) {
     if (o.tri) o.tri[i] = h.tris;
     if (o.vis) o.vis[i] = h.boxes;  // visited == box_tests (kernels.py:115-116)
     if (o.known) o.known[i] = 1;
-    sb += h.boxes;
-    stt += h.tris;
+    sb = h.boxes;
+    stt = h.tris;
   }
   if (a.out.sums) {
     sb = warp_sum(sb);
@@ -179,9 +181,7 @@ int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const int* err, cudaStream_t st) {
   if (n <= 0) return 0;
   TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
-  // one ray per thread for a host-sized batch; a persistent grid-stride grid
-  // for a device-sized queue
-  int grid = count_dev ? num_sms() * 16 : (int)((n + 127) / 128);
+  int grid = (int)((n + 127) / 128);
   ProfScope ps(ray_idx ? P_TRACE_QUEUE : P_TRACE, st);
   if (closest) dispatch_trace<true>(b.stack, grid, st, a);
   else dispatch_trace<false>(b.stack, grid, st, a);

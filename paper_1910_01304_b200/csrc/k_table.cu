@@ -88,6 +88,18 @@ int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, 
   return 0;
 }
 
+int compact_by_flags(Workspace& ws, const int32_t* values, const uint8_t* flags, int64_t n,
+                     int32_t* out, int* count_dev, cudaStream_t st) {
+  size_t b = 0;
+  cub::DeviceSelect::Flagged(nullptr, b, values, flags, out, count_dev, (int)n, st);
+  void* tmp;
+  int rc;
+  if ((rc = ws.get_raw("cbf_tmp", b, &tmp))) return rc;
+  ProfScope ps(P_GROUP, st);
+  HRPP_CK(cub::DeviceSelect::Flagged(tmp, b, values, flags, out, count_dev, (int)n, st));
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // index maintenance
 // ---------------------------------------------------------------------------
@@ -231,112 +243,131 @@ TableDev::~TableDev() {
 // commit the per-segment appends of one wave (or one record batch)
 // ---------------------------------------------------------------------------
 
-struct Trip {
-  long long n_new, reloc, app;
-};
-struct TripSum {
-  __host__ __device__ Trip operator()(const Trip& a, const Trip& b) const {
-    return Trip{a.n_new + b.n_new, a.reloc + b.reloc, a.app + b.app};
-  }
-};
-
-__global__ void k_commit_prepare(const int* nsegs, int64_t n, const int32_t* __restrict__ seg_eid,
-                                 const int32_t* __restrict__ seg_napp,
-                                 const int32_t* __restrict__ e_len, Trip* vals, const int* err) {
-  const int ns = *nsegs;
-  const bool dead = *err != 0;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    Trip v{0, 0, 0};
-    if (s < ns && !dead) {
-      int32_t napp = seg_napp[s], eid = seg_eid[s];
-      if (napp > 0) {
-        v.n_new = eid < 0;
-        v.reloc = (eid >= 0 ? e_len[eid] : 0) + napp;
-        v.app = napp;
-      }
+// Block-wide exclusive scan of two counters (128 threads = 4 warps).
+__device__ __forceinline__ void block_scan2(long long a, long long b, long long& ea, long long& eb,
+                                            long long& ta, long long& tb) {
+  __shared__ long long wa[4], wb[4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long xa = __shfl_up_sync(0xffffffffu, ia, o);
+    long long xb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) {
+      ia += xa;
+      ib += xb;
     }
-    vals[s] = v;
   }
+  if (lane == 31) {
+    wa[w] = ia;
+    wb[w] = ib;
+  }
+  __syncthreads();
+  long long pa = 0, pb = 0;
+  ta = 0;
+  tb = 0;
+  for (int k = 0; k < 4; k++) {
+    if (k < w) {
+      pa += wa[k];
+      pb += wb[k];
+    }
+    ta += wa[k];
+    tb += wb[k];
+  }
+  ea = pa + ia - a;
+  eb = pb + ib - b;
 }
 
-__global__ void k_commit_check(const Trip* vals, const Trip* scan, int64_t n,
-                               const long long* meta, long long max_entries, int* err,
-                               long long* totals) {
-  Trip t = TripSum()(vals[n - 1], scan[n - 1]);
-  totals[0] = t.n_new;
-  totals[1] = t.reloc;
-  totals[2] = t.app;
-  if (*err == 0 && meta[0] + t.n_new > max_entries) *err = 2;  // CapacityExceeded
-}
-
-__global__ void k_commit_apply(const int* nsegs, const int32_t* __restrict__ seg_start,
-                               const unsigned long long* __restrict__ skeys,
-                               const int32_t* __restrict__ seg_eid,
-                               const int32_t* __restrict__ seg_napp,
-                               const int32_t* __restrict__ app, const Trip* __restrict__ scan,
-                               const long long* meta, unsigned long long* e_key,
-                               int64_t* e_off, int32_t* e_len, int32_t* arena,
-                               unsigned long long* idx_keys, int32_t* idx_vals, uint64_t mask,
-                               const int* err) {
+// New entries, relocated list lengths and appended nodes of every touched
+// segment; one atomic per block hands out entry ids and arena ranges (their
+// order varies between runs, every lookup and export result does not).
+__global__ void __launch_bounds__(128) k_commit_count(const int* nsegs, int64_t n,
+                                                      const int32_t* __restrict__ seg_eid,
+                                                      const int32_t* __restrict__ seg_napp,
+                                                      unsigned long long* tot, const int* err) {
   if (*err) return;
   const int ns = *nsegs;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
-    int32_t napp = seg_napp[s];
-    if (napp <= 0) continue;
-    int32_t eid = seg_eid[s];
-    int32_t old_len = 0;
-    int64_t old_off = 0;
-    if (eid >= 0) {
-      old_len = e_len[eid];
-      old_off = e_off[eid];
-    } else {
-      eid = (int32_t)(meta[0] + scan[s].n_new);
-      unsigned long long key = skeys[seg_start[s]];
-      e_key[eid] = key;
-      index_insert(idx_keys, idx_vals, mask, key, eid);
-    }
-    int64_t no = meta[2] + scan[s].reloc;
-    for (int32_t j = 0; j < old_len; j++) arena[no + j] = arena[old_off + j];
-    const int32_t* a = app + seg_start[s];
-    for (int32_t j = 0; j < napp; j++) arena[no + old_len + j] = a[j];
-    e_off[eid] = no;
-    e_len[eid] = old_len + napp;
-  }
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = (s < ns && seg_napp[s] > 0 && seg_eid[s] < 0) ? 1ull : 0ull;
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(tot, v);
 }
 
-__global__ void k_commit_finish(long long* meta, const long long* totals, const int* err) {
+__global__ void k_commit_check(const unsigned long long* tot, const long long* meta,
+                               long long max_entries, int* err) {
+  if (*err == 0 && meta[0] + (long long)tot[0] > max_entries) *err = 2;  // CapacityExceeded
+}
+
+__global__ void __launch_bounds__(128) k_commit_apply(
+    const int* nsegs, int64_t n, const int32_t* __restrict__ seg_start,
+    const unsigned long long* __restrict__ skeys, const int32_t* __restrict__ seg_eid,
+    const int32_t* __restrict__ seg_napp, const int32_t* __restrict__ app, const long long* meta,
+    unsigned long long* e_key, int64_t* e_off, int32_t* e_len, int32_t* arena,
+    unsigned long long* idx_keys, int32_t* idx_vals, uint64_t mask, unsigned long long* cnt,
+    const int* err) {
   if (*err) return;
-  meta[0] += totals[0];
-  meta[1] += totals[2];
-  meta[2] += totals[1];
+  __shared__ long long base_new, base_reloc;
+  const int ns = *nsegs;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t napp = 0, eid = -1, old_len = 0;
+  if (s < ns) {
+    napp = seg_napp[s];
+    if (napp > 0) {
+      eid = seg_eid[s];
+      old_len = eid >= 0 ? e_len[eid] : 0;
+    }
+  }
+  const long long is_new = napp > 0 && eid < 0;
+  const long long reloc = napp > 0 ? old_len + napp : 0;
+  long long ex_new, ex_reloc, t_new, t_reloc;
+  block_scan2(is_new, reloc, ex_new, ex_reloc, t_new, t_reloc);
+  unsigned long long app_sum = warp_sum((unsigned long long)napp);
+  if ((threadIdx.x & 31) == 0 && app_sum) atomicAdd(cnt + 2, app_sum);
+  if (threadIdx.x == 0) {
+    base_new = t_new ? (long long)atomicAdd(cnt, (unsigned long long)t_new) : 0;
+    base_reloc = t_reloc ? (long long)atomicAdd(cnt + 1, (unsigned long long)t_reloc) : 0;
+  }
+  __syncthreads();
+  if (napp <= 0) return;
+  const int64_t old_off = eid >= 0 ? e_off[eid] : 0;
+  if (eid < 0) {
+    eid = (int32_t)(meta[0] + base_new + ex_new);
+    const unsigned long long key = skeys[seg_start[s]];
+    e_key[eid] = key;
+    index_insert(idx_keys, idx_vals, mask, key, eid);
+  }
+  const int64_t no = meta[2] + base_reloc + ex_reloc;
+  for (int32_t j = 0; j < old_len; j++) arena[no + j] = arena[old_off + j];
+  const int32_t* a = app + seg_start[s];
+  for (int32_t j = 0; j < napp; j++) arena[no + old_len + j] = a[j];
+  e_off[eid] = no;
+  e_len[eid] = old_len + napp;
+}
+
+__global__ void k_commit_finish(long long* meta, const unsigned long long* cnt, const int* err) {
+  if (*err) return;
+  meta[0] += (long long)cnt[0];
+  meta[1] += (long long)cnt[2];
+  meta[2] += (long long)cnt[1];
 }
 
 int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
                  int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st) {
-  Trip *vals, *scan;
-  long long* totals;
+  unsigned long long* cnt;  // [0] new entries [1] relocated nodes [2] appended nodes [3] count
   int rc;
-  if ((rc = t.ws.get("m_vals", n, &vals))) return rc;
-  if ((rc = t.ws.get("m_scan", n, &scan))) return rc;
-  if ((rc = t.ws.get("m_tot", 4, &totals))) return rc;
-  int grid = grid_for(n, 256, num_sms() * 8);
+  if ((rc = t.ws.get("m_cnt", 4, &cnt))) return rc;
+  const int grid = (int)((n + 127) / 128);
   ProfScope ps(P_COMMIT, st);
-  k_commit_prepare<<<grid, 256, 0, st>>>(seg.nsegs, n, seg_eid, seg_napp, t.e_len, vals, err);
+  HRPP_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 4, st));
+  k_commit_count<<<grid, 128, 0, st>>>(seg.nsegs, n, seg_eid, seg_napp, cnt + 3, err);
   HRPP_LAUNCHED();
-  size_t b = 0;
-  cub::DeviceScan::ExclusiveScan(nullptr, b, vals, scan, TripSum(), Trip{0, 0, 0}, (int)n, st);
-  void* tmp;
-  if ((rc = t.ws.get_raw("m_tmp", b, &tmp))) return rc;
-  HRPP_CK(cub::DeviceScan::ExclusiveScan(tmp, b, vals, scan, TripSum(), Trip{0, 0, 0}, (int)n,
-                                         st));
-  k_commit_check<<<1, 1, 0, st>>>(vals, scan, n, t.meta, (long long)t.max_entries, err, totals);
+  k_commit_check<<<1, 1, 0, st>>>(cnt + 3, t.meta, (long long)t.max_entries, err);
   HRPP_LAUNCHED();
-  k_commit_apply<<<grid, 256, 0, st>>>(seg.nsegs, seg.seg_start, seg.skeys, seg_eid, seg_napp,
-                                       app, scan, t.meta, t.e_key, t.e_off, t.e_len, t.arena,
-                                       t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, err);
+  k_commit_apply<<<grid, 128, 0, st>>>(seg.nsegs, n, seg.seg_start, seg.skeys, seg_eid, seg_napp,
+                                       app, t.meta, t.e_key, t.e_off, t.e_len, t.arena,
+                                       t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, cnt, err);
   HRPP_LAUNCHED();
-  k_commit_finish<<<1, 1, 0, st>>>(t.meta, totals, err);
+  k_commit_finish<<<1, 1, 0, st>>>(t.meta, cnt, err);
   HRPP_LAUNCHED();
   return 0;
 }
