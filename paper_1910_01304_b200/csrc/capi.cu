@@ -481,7 +481,7 @@ int hrpp_table_create(int precision, int go_up_level, int kind, int64_t max_entr
   t->closest = kind == HRPP_CLOSEST_HIT;
   t->max_entries = max_entries;
   t->ws.device = device;
-  int rc = t->reserve(0, 0);
+  int rc = t->reserve(0, 0, 0);
   if (rc) {
     delete t;
     return rc;
@@ -500,8 +500,7 @@ int hrpp_table_clear(hrpp_table_t t) {
   CHECK_ARG(t, "null table");
   HRPP_CK(cudaSetDevice(t->device));
   HRPP_CK(cudaMemset(t->meta, 0, sizeof(long long) * 4));
-  if (t->idx_keys)
-    HRPP_CK(cudaMemset(t->idx_keys, 0xFF, sizeof(unsigned long long) * t->idx_cap));
+  if (t->idx) HRPP_CK(cudaMemset(t->idx, 0xFF, sizeof(Bucket) * t->idx_cap));
   t->n_entries = t->stored = t->arena_used = 0;
   return HRPP_OK;
 }

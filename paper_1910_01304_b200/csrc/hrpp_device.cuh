@@ -206,14 +206,20 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-__device__ __forceinline__ int32_t index_lookup(const unsigned long long* __restrict__ keys,
-                                                const int32_t* __restrict__ vals, uint64_t mask,
+// One 16-B bucket per probe: {key, entry id}.
+struct __align__(16) Bucket {
+  unsigned long long key;
+  int32_t val;
+  int32_t pad;
+};
+
+__device__ __forceinline__ int32_t index_lookup(const Bucket* __restrict__ idx, uint64_t mask,
                                                 uint64_t key) {
   uint64_t h = mix64(key) & mask;
   for (;;) {
-    unsigned long long k = keys[h];
-    if (k == key) return vals[h];
-    if (k == kEmptyKey) return -1;
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(idx + h);
+    if (b.x == key) return (int32_t)(b.y & 0xffffffffull);
+    if (b.x == kEmptyKey) return -1;
     h = (h + 1) & mask;
   }
 }

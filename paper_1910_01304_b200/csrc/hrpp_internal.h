@@ -91,8 +91,7 @@ struct TableDev {
   bool closest = true;
   int64_t max_entries = 1 << 26;
   // hash index: key -> entry id
-  unsigned long long* idx_keys = nullptr;
-  int32_t* idx_vals = nullptr;
+  Bucket* idx = nullptr;
   int64_t idx_cap = 0;
   // entries (creation order), node lists in the arena
   unsigned long long* e_key = nullptr;
@@ -111,7 +110,8 @@ struct TableDev {
   int64_t pending = 0;
   Workspace ws;
   ~TableDev();
-  int reserve(int64_t extra_rays, cudaStream_t st);  // capacity for a wave of extra_rays
+  // capacity for up to extra_entries new entries and extra_nodes new nodes
+  int reserve(int64_t extra_entries, int64_t extra_nodes, cudaStream_t st);
 };
 
 // ---- launchers (return HRPP status) ----

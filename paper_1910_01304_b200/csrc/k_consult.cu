@@ -34,8 +34,8 @@ int g_consult_short = 32;  // segments up to this many rays are replayed by one 
 
 enum { S_RAYS, S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG };
 
-// Running eval_entry result of one ray (by sorted position): 32 bytes, two
-// 16-B accesses.  `applied` = number of entry nodes already folded.
+// Running eval_entry result of one ray (by ray index): 32 bytes, two 16-B
+// accesses.  `applied` = number of entry nodes already folded.
 struct __align__(16) RayState {
   double t;
   int32_t slot, leaf;
@@ -58,8 +58,7 @@ struct ConsultArgs {
   const int32_t* seg_start;
   const int32_t* seg_id;
   const int* nsegs;
-  const unsigned long long* idx_keys;
-  const int32_t* idx_vals;
+  const Bucket* idx;
   uint64_t mask;
   const int64_t* e_off;
   const int32_t* e_len;
@@ -72,7 +71,9 @@ struct ConsultArgs {
   int32_t* seg_cursor;
   int32_t* app;      // appended nodes of segment s live at app[seg_start[s] ...]
   int32_t* app_ray;  // ray index that triggered each append (deferred mode)
-  RayState* state;   // per sorted position
+  RayState* state;   // per ray index
+  int32_t* seg_of_ray;  // per ray index: key segment
+  int32_t* pos_of_ray;  // per ray index: sorted position
   // full-traversal results by ray index (baseline in limit mode)
   const uint8_t* f_found;
   const double* f_t;
@@ -205,7 +206,7 @@ __global__ void k_seg_lookup(ConsultArgs a, int64_t n) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int32_t beg = a.seg_start[s];
-    const int32_t eid = index_lookup(a.idx_keys, a.idx_vals, a.mask, a.skeys[beg]);
+    const int32_t eid = index_lookup(a.idx, a.mask, a.skeys[beg]);
     a.seg_eid[s] = eid;
     a.seg_exoff[s] = eid >= 0 ? a.e_off[eid] : 0;
     a.seg_exlen[s] = eid >= 0 ? a.e_len[eid] : 0;
@@ -228,18 +229,19 @@ __device__ __forceinline__ bool in_list(const ConsultArgs& a, int64_t off, int32
   return false;
 }
 
+// The stable sort keeps rays of one key in ray order, so within a segment
+// "first in the replay" is "smallest ray index".
 __global__ void k_first_append(ConsultArgs a, int64_t n) {
   if (*a.err) return;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const RayState st = a.state[p];
-    const int32_t s = a.seg_id[p] - 1;
-    const int32_t ex_len = a.seg_exlen[s];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const RayState st = a.state[i];
+    const int32_t s = a.seg_of_ray[i];
+    const int32_t ex_len = st.applied;  // eval0 folded exactly the wave-start entry
     if (ex_len > 0 && st.found) continue;  // TP against the wave-start entry
-    const int32_t idx = a.sidx[p];
-    if (!a.f_found[idx]) continue;
-    if (!in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[idx]]))
-      atomicMin(a.seg_f1 + s, (int32_t)p);
+    if (!a.f_found[i]) continue;
+    if (!in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[i]]))
+      atomicMin(a.seg_f1 + s, (int32_t)i);
   }
 }
 
@@ -247,26 +249,20 @@ template <bool CLOSEST, bool LIVE>
 __global__ void __launch_bounds__(128) k_finalize(ConsultArgs a, int64_t n) {
   if (*a.err) return;
   Tally c;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = a.seg_id[p] - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = a.seg_of_ray[i];
     const int32_t f1 = a.seg_f1[s];
-    const int32_t beg = a.seg_start[s];
-    if (p > f1) continue;  // after the first append: replayed
+    if (i > f1) continue;  // after the first append: replayed
     Hit acc;
-    int32_t applied;
-    load_state(a, (int32_t)p, acc, applied);
-    const int32_t ex_len = a.seg_exlen[s];
-    const int32_t idx = a.sidx[p];
-    if (ex_len > 0 && acc.found) commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
-    else commit_miss<LIVE>(a, c, idx, acc, ex_len == 0);
-    if (p == f1) {  // the first record(key, anc[leaf]) of this segment
-      a.app[beg] = a.anc[a.f_leaf[idx]];
-      a.app_ray[beg] = idx;
-      a.seg_napp[s] = 1;
-      a.seg_cursor[s] = f1 + 1;
-    } else if (p == beg && f1 == 0x7fffffff) {
-      a.seg_cursor[s] = a.seg_start[s + 1];  // no append: the segment is done
+    int32_t ex_len;
+    load_state(a, (int32_t)i, acc, ex_len);
+    if (ex_len > 0 && acc.found) commit_tp<CLOSEST, LIVE>(a, c, (int32_t)i, acc);
+    else commit_miss<LIVE>(a, c, (int32_t)i, acc, ex_len == 0);
+    if (i == f1) {  // the first record(key, anc[leaf]) of this segment
+      const int32_t beg = a.seg_start[s];
+      a.app[beg] = a.anc[a.f_leaf[i]];
+      a.app_ray[beg] = (int32_t)i;
     }
   }
   long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
@@ -279,20 +275,48 @@ __global__ void __launch_bounds__(128) k_finalize(ConsultArgs a, int64_t n) {
   }
 }
 
+// Replay cursor per segment: right after its first append, or done.
+__global__ void k_seg_cursor(ConsultArgs a) {
+  const int ns = *a.nsegs;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t f1 = a.seg_f1[s];
+    if (f1 == 0x7fffffff) {
+      a.seg_cursor[s] = a.seg_start[s + 1];
+      a.seg_napp[s] = 0;
+    } else {
+      a.seg_cursor[s] = a.pos_of_ray[f1] + 1;
+      a.seg_napp[s] = 1;
+    }
+  }
+}
+
+// Ray -> (segment, sorted position), scattered once per wave.
+__global__ void k_seg_scatter(ConsultArgs a, int64_t n) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = a.sidx[p];
+    a.seg_of_ray[i] = a.seg_id[p] - 1;
+    a.pos_of_ray[i] = (int32_t)p;
+  }
+}
+
+// Every ray against the entry as it stood at the start of the wave; ray
+// order, so ray, state and flag accesses are coalesced.
 template <bool CLOSEST, int STACK>
 __global__ void __launch_bounds__(128) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
   if (*a.err) return;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = a.seg_id[p] - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = a.seg_of_ray[i];
     const int32_t ex_len = a.seg_exlen[s];
     Hit acc = empty_entry_result(CLOSEST);
     if (ex_len > 0) {
-      const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, a.sidx[p]);
+      const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
       catch_up<CLOSEST, STACK>(a, r, acc, 0, ex_len, a.seg_exoff[s], ex_len, nullptr);
     }
-    store_state(a, (int32_t)p, acc, ex_len);
-    if (mark_need && !(ex_len > 0 && acc.found)) a.need[a.sidx[p]] = 1;
+    store_state(a, (int32_t)i, acc, ex_len);
+    if (mark_need) a.need[i] = !(ex_len > 0 && acc.found);
   }
 }
 
@@ -310,11 +334,11 @@ __device__ void speculate_rest(const ConsultArgs& a, int32_t from, int32_t end, 
     const int32_t idx = a.sidx[j];
     Hit acc;
     int32_t applied;
-    load_state(a, j, acc, applied);
+    load_state(a, idx, acc, applied);
     if (applied < L && (CLOSEST || !acc.found)) {
       const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
       catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
-      store_state(a, j, acc, L);
+      store_state(a, idx, acc, L);
     }
     if (!(L > 0 && acc.found) && !a.f_known[idx]) a.need[idx] = 1;
   }
@@ -333,7 +357,7 @@ __device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, i
     const int32_t idx = a.sidx[j];
     Hit acc;
     int32_t applied;
-    load_state(a, j, acc, applied);
+    load_state(a, idx, acc, applied);
     const int32_t L = ex_len + napp;
     if (applied < L && (CLOSEST || !acc.found)) {
       const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
@@ -345,7 +369,7 @@ __device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, i
     }
     if (LIVE && !a.f_known[idx]) {  // suspend until its full traversal is known
       a.need[idx] = 1;
-      store_state(a, j, acc, L);
+      store_state(a, idx, acc, L);
       if (a.spec >= 2) speculate_rest<CLOSEST, STACK>(a, j + 1, end, L, ex_off, ex_len, app);
       break;
     }
@@ -382,7 +406,7 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
     const int32_t idx = valid ? a.sidx[pos] : 0;
     Hit acc = empty_entry_result(CLOSEST);
     int32_t applied = 0;
-    if (valid) load_state(a, pos, acc, applied);
+    if (valid) load_state(a, idx, acc, applied);
     int32_t L = ex_len + napp;
     const bool fknown = valid && (!LIVE || a.f_known[idx]);
     int32_t cnode = -1;
@@ -403,17 +427,17 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
       if (f == 32) break;
       if (LIVE && !__shfl_sync(kFull, fknown, f)) {  // suspend at ray f
         if (lane == f || (a.spec >= 1 && need && !fknown)) a.need[idx] = 1;
-        if (valid && lane >= f) store_state(a, pos, acc, applied);
+        if (valid && lane >= f) store_state(a, idx, acc, applied);
         if (a.spec >= 2) {
           for (int32_t t2 = tb + 32 + lane; t2 < end; t2 += 32) {
             const int32_t i2 = a.sidx[t2];
             Hit a2;
             int32_t ap2;
-            load_state(a, t2, a2, ap2);
+            load_state(a, i2, a2, ap2);
             if (ap2 < L && (CLOSEST || !a2.found)) {
               const Ray r2 = make_ray(a.O, a.D, a.tmin, a.tmax, i2);
               catch_up<CLOSEST, STACK>(a, r2, a2, ap2, L, ex_off, ex_len, app);
-              store_state(a, t2, a2, L);
+              store_state(a, i2, a2, L);
             }
             if (!(L > 0 && a2.found) && !a.f_known[i2]) a.need[i2] = 1;
           }
@@ -543,6 +567,8 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
     else k_finalize<false, false><<<grid, 128, 0, st>>>(a, n);
   }
   HRPP_LAUNCHED();
+  k_seg_cursor<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a);
+  HRPP_LAUNCHED();
   return 0;
 }
 
@@ -551,11 +577,16 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   const int64_t n = c.n;
   if (n <= 0) return 0;
   int rc;
-  if ((rc = t.reserve(n, st))) return rc;
   const int32_t* anc;
   if ((rc = const_cast<BvhDev&>(b).ancestor_lut(t.go_up, &anc))) return rc;
   Segments seg;
   if ((rc = group_by_key(t.ws, keys, n, &seg, st))) return rc;
+  // new entries <= key segments: read the segment count once so the hash
+  // index stays sized to the table (L2-resident for c1-c3 tables), not to the wave
+  int nsegs_h = 0;
+  HRPP_CK(cudaMemcpyAsync(&nsegs_h, seg.nsegs, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HRPP_CK(cudaStreamSynchronize(st));
+  if ((rc = t.reserve(nsegs_h, n, st))) return rc;
   Workspace& ws = t.ws;
   ConsultArgs a{};
   a.nodes = b.nodes;
@@ -571,8 +602,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   a.seg_start = seg.seg_start;
   a.seg_id = seg.seg_id;
   a.nsegs = seg.nsegs;
-  a.idx_keys = t.idx_keys;
-  a.idx_vals = t.idx_vals;
+  a.idx = t.idx;
   a.mask = (uint64_t)t.idx_cap - 1;
   a.e_off = t.e_off;
   a.e_len = t.e_len;
@@ -583,12 +613,15 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       (rc = ws.get("k_exlen", n, &a.seg_exlen)) || (rc = ws.get("k_napp", n, &a.seg_napp)) ||
       (rc = ws.get("k_cursor", n, &a.seg_cursor)) || (rc = ws.get("k_app", n, &a.app)) ||
       (rc = ws.get("k_appray", n, &a.app_ray)) || (rc = ws.get("k_state", n, &a.state)) ||
-      (rc = ws.get("k_f1", n, &a.seg_f1)))
+      (rc = ws.get("k_f1", n, &a.seg_f1)) || (rc = ws.get("k_segofray", n, &a.seg_of_ray)) ||
+      (rc = ws.get("k_posofray", n, &a.pos_of_ray)))
     return rc;
   const int grid = (int)((n + 127) / 128);  // thread t owns segment t (nsegs <= n)
   {
     ProfScope ps(P_CONSULT, st);
     k_seg_lookup<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a, n);
+    HRPP_LAUNCHED();
+    k_seg_scatter<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
     HRPP_LAUNCHED();
   }
   const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;

@@ -104,14 +104,13 @@ int compact_by_flags(Workspace& ws, const int32_t* values, const uint8_t* flags,
 // index maintenance
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void index_insert(unsigned long long* keys, int32_t* vals,
-                                             uint64_t mask, unsigned long long key,
+__device__ __forceinline__ void index_insert(Bucket* idx, uint64_t mask, unsigned long long key,
                                              int32_t id) {
   uint64_t h = mix64(key) & mask;
   for (;;) {
-    unsigned long long prev = atomicCAS(keys + h, kEmptyKey, key);
+    unsigned long long prev = atomicCAS(&idx[h].key, kEmptyKey, key);
     if (prev == kEmptyKey || prev == key) {
-      vals[h] = id;
+      idx[h].val = id;
       return;
     }
     h = (h + 1) & mask;
@@ -119,10 +118,10 @@ __device__ __forceinline__ void index_insert(unsigned long long* keys, int32_t* 
 }
 
 __global__ void k_rehash(const unsigned long long* __restrict__ e_key, int64_t n_entries,
-                         unsigned long long* keys, int32_t* vals, uint64_t mask) {
+                         Bucket* idx, uint64_t mask) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_entries;
        e += (int64_t)gridDim.x * blockDim.x)
-    index_insert(keys, vals, mask, e_key[e], (int32_t)e);
+    index_insert(idx, mask, e_key[e], (int32_t)e);
 }
 
 __global__ void k_len_to_i64(const int32_t* __restrict__ len, int64_t n, long long* out) {
@@ -162,13 +161,13 @@ static int grow(T** p, int64_t old_count, int64_t new_count, cudaStream_t st) {
   return 0;
 }
 
-int TableDev::reserve(int64_t extra, cudaStream_t st) {
+int TableDev::reserve(int64_t extra_e, int64_t extra, cudaStream_t st) {
   int rc;
   if (!meta) {
     HRPP_CK(cudaMalloc(&meta, sizeof(long long) * 4));
     HRPP_CK(cudaMemsetAsync(meta, 0, sizeof(long long) * 4, st));
   }
-  int64_t need_e = n_entries + extra + 16;
+  int64_t need_e = n_entries + extra_e + 16;
   if (e_cap < need_e) {
     int64_t nc = need_e > 2 * e_cap ? need_e : 2 * e_cap;
     if ((rc = grow(&e_key, n_entries, nc, st))) return rc;
@@ -178,18 +177,16 @@ int TableDev::reserve(int64_t extra, cudaStream_t st) {
   }
   int64_t need_idx = next_pow2(2 * need_e);
   if (idx_cap < need_idx) {
-    if (idx_keys) {
+    if (idx) {
       HRPP_CK(cudaStreamSynchronize(st));
-      HRPP_CK(cudaFree(idx_keys));
-      HRPP_CK(cudaFree(idx_vals));
+      HRPP_CK(cudaFree(idx));
     }
-    HRPP_CK(cudaMalloc(&idx_keys, sizeof(unsigned long long) * need_idx));
-    HRPP_CK(cudaMalloc(&idx_vals, sizeof(int32_t) * need_idx));
-    HRPP_CK(cudaMemsetAsync(idx_keys, 0xFF, sizeof(unsigned long long) * need_idx, st));
+    HRPP_CK(cudaMalloc(&idx, sizeof(Bucket) * need_idx));
+    HRPP_CK(cudaMemsetAsync(idx, 0xFF, sizeof(Bucket) * need_idx, st));
     idx_cap = need_idx;
     if (n_entries) {
       k_rehash<<<grid_for(n_entries, 256, num_sms() * 8), 256, 0, st>>>(
-          e_key, n_entries, idx_keys, idx_vals, (uint64_t)idx_cap - 1);
+          e_key, n_entries, idx, (uint64_t)idx_cap - 1);
       HRPP_LAUNCHED();
     }
   }
@@ -230,8 +227,7 @@ int TableDev::reserve(int64_t extra, cudaStream_t st) {
 }
 
 TableDev::~TableDev() {
-  cudaFree(idx_keys);
-  cudaFree(idx_vals);
+  cudaFree(idx);
   cudaFree(e_key);
   cudaFree(e_off);
   cudaFree(e_len);
@@ -278,38 +274,28 @@ __device__ __forceinline__ void block_scan2(long long a, long long b, long long&
   eb = pb + ib - b;
 }
 
-// New entries, relocated list lengths and appended nodes of every touched
-// segment; one atomic per block hands out entry ids and arena ranges (their
-// order varies between runs, every lookup and export result does not).
-__global__ void __launch_bounds__(128) k_commit_count(const int* nsegs, int64_t n,
-                                                      const int32_t* __restrict__ seg_eid,
-                                                      const int32_t* __restrict__ seg_napp,
-                                                      unsigned long long* tot, const int* err) {
-  if (*err) return;
-  const int ns = *nsegs;
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long v = (s < ns && seg_napp[s] > 0 && seg_eid[s] < 0) ? 1ull : 0ull;
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(tot, v);
-}
+// Commit of the touched segments: per block (128 segments) the counts of new
+// entries, relocated list nodes and appended nodes; an exclusive scan over
+// the block totals; then every block places its entries and lists.  No
+// contended atomics; entry ids and arena layout are deterministic.
+struct Tot3 {
+  long long n_new, reloc, app;
+};
+struct Tot3Sum {
+  __host__ __device__ Tot3 operator()(const Tot3& a, const Tot3& b) const {
+    return Tot3{a.n_new + b.n_new, a.reloc + b.reloc, a.app + b.app};
+  }
+};
 
-__global__ void k_commit_check(const unsigned long long* tot, const long long* meta,
-                               long long max_entries, int* err) {
-  if (*err == 0 && meta[0] + (long long)tot[0] > max_entries) *err = 2;  // CapacityExceeded
-}
-
-__global__ void __launch_bounds__(128) k_commit_apply(
-    const int* nsegs, int64_t n, const int32_t* __restrict__ seg_start,
-    const unsigned long long* __restrict__ skeys, const int32_t* __restrict__ seg_eid,
-    const int32_t* __restrict__ seg_napp, const int32_t* __restrict__ app, const long long* meta,
-    unsigned long long* e_key, int64_t* e_off, int32_t* e_len, int32_t* arena,
-    unsigned long long* idx_keys, int32_t* idx_vals, uint64_t mask, unsigned long long* cnt,
-    const int* err) {
-  if (*err) return;
-  __shared__ long long base_new, base_reloc;
-  const int ns = *nsegs;
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int32_t napp = 0, eid = -1, old_len = 0;
+__device__ __forceinline__ void seg_commit_counts(const int ns, int64_t s,
+                                                  const int32_t* __restrict__ seg_eid,
+                                                  const int32_t* __restrict__ seg_napp,
+                                                  const int32_t* __restrict__ e_len,
+                                                  int32_t& napp, int32_t& eid,
+                                                  int32_t& old_len) {
+  napp = 0;
+  eid = -1;
+  old_len = 0;
   if (s < ns) {
     napp = seg_napp[s];
     if (napp > 0) {
@@ -317,26 +303,59 @@ __global__ void __launch_bounds__(128) k_commit_apply(
       old_len = eid >= 0 ? e_len[eid] : 0;
     }
   }
-  const long long is_new = napp > 0 && eid < 0;
-  const long long reloc = napp > 0 ? old_len + napp : 0;
+}
+
+__global__ void __launch_bounds__(128) k_commit_count(const int* nsegs,
+                                                      const int32_t* __restrict__ seg_eid,
+                                                      const int32_t* __restrict__ seg_napp,
+                                                      const int32_t* __restrict__ e_len,
+                                                      Tot3* block_tot, const int* err) {
+  if (*err) return;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t napp, eid, old_len;
+  seg_commit_counts(*nsegs, s, seg_eid, seg_napp, e_len, napp, eid, old_len);
   long long ex_new, ex_reloc, t_new, t_reloc;
-  block_scan2(is_new, reloc, ex_new, ex_reloc, t_new, t_reloc);
-  unsigned long long app_sum = warp_sum((unsigned long long)napp);
-  if ((threadIdx.x & 31) == 0 && app_sum) atomicAdd(cnt + 2, app_sum);
-  if (threadIdx.x == 0) {
-    base_new = t_new ? (long long)atomicAdd(cnt, (unsigned long long)t_new) : 0;
-    base_reloc = t_reloc ? (long long)atomicAdd(cnt + 1, (unsigned long long)t_reloc) : 0;
-  }
+  block_scan2(napp > 0 && eid < 0, napp > 0 ? old_len + napp : 0, ex_new, ex_reloc, t_new,
+              t_reloc);
+  __shared__ long long wapp[4];
+  long long a = warp_sum((long long)napp);
+  if ((threadIdx.x & 31) == 0) wapp[threadIdx.x >> 5] = a;
   __syncthreads();
+  if (threadIdx.x == 0)
+    block_tot[blockIdx.x] = Tot3{t_new, t_reloc, wapp[0] + wapp[1] + wapp[2] + wapp[3]};
+}
+
+__global__ void k_commit_check(const Tot3* block_tot, const Tot3* block_off, int nblocks,
+                               const long long* meta, long long max_entries, int* err,
+                               Tot3* total) {
+  const Tot3 t = Tot3Sum()(block_off[nblocks - 1], block_tot[nblocks - 1]);
+  *total = t;
+  if (*err == 0 && meta[0] + t.n_new > max_entries) *err = 2;  // CapacityExceeded
+}
+
+__global__ void __launch_bounds__(128) k_commit_apply(
+    const int* nsegs, const int32_t* __restrict__ seg_start,
+    const unsigned long long* __restrict__ skeys, const int32_t* __restrict__ seg_eid,
+    const int32_t* __restrict__ seg_napp, const int32_t* __restrict__ app, const long long* meta,
+    unsigned long long* e_key, int64_t* e_off, int32_t* e_len, int32_t* arena, Bucket* idx,
+    uint64_t mask, const Tot3* __restrict__ block_off, const int* err) {
+  if (*err) return;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t napp, eid, old_len;
+  seg_commit_counts(*nsegs, s, seg_eid, seg_napp, e_len, napp, eid, old_len);
+  long long ex_new, ex_reloc, t_new, t_reloc;
+  block_scan2(napp > 0 && eid < 0, napp > 0 ? old_len + napp : 0, ex_new, ex_reloc, t_new,
+              t_reloc);
   if (napp <= 0) return;
+  const Tot3 base = block_off[blockIdx.x];
   const int64_t old_off = eid >= 0 ? e_off[eid] : 0;
   if (eid < 0) {
-    eid = (int32_t)(meta[0] + base_new + ex_new);
+    eid = (int32_t)(meta[0] + base.n_new + ex_new);
     const unsigned long long key = skeys[seg_start[s]];
     e_key[eid] = key;
-    index_insert(idx_keys, idx_vals, mask, key, eid);
+    index_insert(idx, mask, key, eid);
   }
-  const int64_t no = meta[2] + base_reloc + ex_reloc;
+  const int64_t no = meta[2] + base.reloc + ex_reloc;
   for (int32_t j = 0; j < old_len; j++) arena[no + j] = arena[old_off + j];
   const int32_t* a = app + seg_start[s];
   for (int32_t j = 0; j < napp; j++) arena[no + old_len + j] = a[j];
@@ -344,30 +363,38 @@ __global__ void __launch_bounds__(128) k_commit_apply(
   e_len[eid] = old_len + napp;
 }
 
-__global__ void k_commit_finish(long long* meta, const unsigned long long* cnt, const int* err) {
+__global__ void k_commit_finish(long long* meta, const Tot3* total, const int* err) {
   if (*err) return;
-  meta[0] += (long long)cnt[0];
-  meta[1] += (long long)cnt[2];
-  meta[2] += (long long)cnt[1];
+  meta[0] += total->n_new;
+  meta[1] += total->app;
+  meta[2] += total->reloc;
 }
 
 int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
                  int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st) {
-  unsigned long long* cnt;  // [0] new entries [1] relocated nodes [2] appended nodes [3] count
+  const int nblocks = (int)((n + 127) / 128);
+  Tot3 *btot, *boff, *total;
   int rc;
-  if ((rc = t.ws.get("m_cnt", 4, &cnt))) return rc;
-  const int grid = (int)((n + 127) / 128);
+  if ((rc = t.ws.get("m_btot", nblocks, &btot)) || (rc = t.ws.get("m_boff", nblocks, &boff)) ||
+      (rc = t.ws.get("m_total", 1, &total)))
+    return rc;
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, b, btot, boff, Tot3Sum(), Tot3{0, 0, 0}, nblocks, st);
+  void* tmp;
+  if ((rc = t.ws.get_raw("m_tmp", b, &tmp))) return rc;
   ProfScope ps(P_COMMIT, st);
-  HRPP_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 4, st));
-  k_commit_count<<<grid, 128, 0, st>>>(seg.nsegs, n, seg_eid, seg_napp, cnt + 3, err);
+  k_commit_count<<<nblocks, 128, 0, st>>>(seg.nsegs, seg_eid, seg_napp, t.e_len, btot, err);
   HRPP_LAUNCHED();
-  k_commit_check<<<1, 1, 0, st>>>(cnt + 3, t.meta, (long long)t.max_entries, err);
+  HRPP_CK(cub::DeviceScan::ExclusiveScan(tmp, b, btot, boff, Tot3Sum(), Tot3{0, 0, 0}, nblocks,
+                                         st));
+  k_commit_check<<<1, 1, 0, st>>>(btot, boff, nblocks, t.meta, (long long)t.max_entries, err,
+                                  total);
   HRPP_LAUNCHED();
-  k_commit_apply<<<grid, 128, 0, st>>>(seg.nsegs, n, seg.seg_start, seg.skeys, seg_eid, seg_napp,
-                                       app, t.meta, t.e_key, t.e_off, t.e_len, t.arena,
-                                       t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, cnt, err);
+  k_commit_apply<<<nblocks, 128, 0, st>>>(seg.nsegs, seg.seg_start, seg.skeys, seg_eid, seg_napp,
+                                          app, t.meta, t.e_key, t.e_off, t.e_len, t.arena, t.idx,
+                                          (uint64_t)t.idx_cap - 1, boff, err);
   HRPP_LAUNCHED();
-  k_commit_finish<<<1, 1, 0, st>>>(t.meta, cnt, err);
+  k_commit_finish<<<1, 1, 0, st>>>(t.meta, total, err);
   HRPP_LAUNCHED();
   return 0;
 }
@@ -467,15 +494,14 @@ int table_collect_pending(TableDev& t, const Segments& seg, int64_t n, const int
 __global__ void k_record_seg(const int* nsegs, const int32_t* __restrict__ seg_start,
                              const unsigned long long* __restrict__ skeys,
                              const int32_t* __restrict__ sidx, const int32_t* __restrict__ nodes,
-                             const unsigned long long* __restrict__ idx_keys,
-                             const int32_t* __restrict__ idx_vals, uint64_t mask,
+                             const Bucket* __restrict__ idx, uint64_t mask,
                              const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_len,
                              const int32_t* __restrict__ arena, int32_t* app, int32_t* seg_eid,
                              int32_t* seg_napp, uint8_t* inserted) {
   const int ns = *nsegs;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
     int32_t beg = seg_start[s], end = seg_start[s + 1];
-    int32_t eid = index_lookup(idx_keys, idx_vals, mask, skeys[beg]);
+    int32_t eid = index_lookup(idx, mask, skeys[beg]);
     int64_t off = eid >= 0 ? e_off[eid] : 0;
     int32_t len = eid >= 0 ? e_len[eid] : 0;
     int32_t* ap = app + beg;
@@ -497,7 +523,7 @@ __global__ void k_record_seg(const int* nsegs, const int32_t* __restrict__ seg_s
 int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_t n,
                  uint8_t* inserted, int* err, cudaStream_t st) {
   int rc;
-  if ((rc = t.reserve(n, st))) return rc;
+  if ((rc = t.reserve(n, n, st))) return rc;
   Segments seg;
   if ((rc = group_by_key(t.ws, keys, n, &seg, st))) return rc;
   int32_t *app, *seg_eid, *seg_napp;
@@ -505,7 +531,7 @@ int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_
   if ((rc = t.ws.get("r_eid", n, &seg_eid))) return rc;
   if ((rc = t.ws.get("r_napp", n, &seg_napp))) return rc;
   k_record_seg<<<grid_for(n, 128, num_sms() * 16), 128, 0, st>>>(
-      seg.nsegs, seg.seg_start, seg.skeys, seg.sidx, nodes, t.idx_keys, t.idx_vals,
+      seg.nsegs, seg.seg_start, seg.skeys, seg.sidx, nodes, t.idx,
       (uint64_t)t.idx_cap - 1, t.e_off, t.e_len, t.arena, app, seg_eid, seg_napp, inserted);
   HRPP_LAUNCHED();
   return table_commit(t, seg, n, seg_eid, seg_napp, app, err, st);
@@ -572,11 +598,10 @@ int table_export(TableDev& t, uint64_t* keys_h, int64_t* offs_h, int32_t* nodes_
   return 0;
 }
 
-__global__ void k_lookup1(const unsigned long long* __restrict__ idx_keys,
-                          const int32_t* __restrict__ idx_vals, uint64_t mask, uint64_t key,
+__global__ void k_lookup1(const Bucket* __restrict__ idx, uint64_t mask, uint64_t key,
                           const int64_t* __restrict__ e_off, const int32_t* __restrict__ e_len,
                           long long* out) {
-  int32_t e = idx_keys ? index_lookup(idx_keys, idx_vals, mask, key) : -1;
+  int32_t e = idx ? index_lookup(idx, mask, key) : -1;
   out[0] = e >= 0 ? e_off[e] : 0;
   out[1] = e >= 0 ? e_len[e] : 0;
 }
@@ -587,7 +612,7 @@ int table_lookup1(TableDev& t, uint64_t key, int32_t* nodes_h, int64_t cap, int6
   long long* out;
   int rc;
   if ((rc = t.ws.get("l_out", 2, &out))) return rc;
-  k_lookup1<<<1, 1>>>(t.idx_keys, t.idx_vals, (uint64_t)t.idx_cap - 1, key, t.e_off, t.e_len, out);
+  k_lookup1<<<1, 1>>>(t.idx, (uint64_t)t.idx_cap - 1, key, t.e_off, t.e_len, out);
   HRPP_LAUNCHED();
   long long h[2];
   HRPP_CK(cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost));
@@ -623,8 +648,7 @@ struct PredictArgs {
   const DNode* nodes;
   const DTri* tris;
   const int32_t* depth;
-  const unsigned long long* idx_keys;
-  const int32_t* idx_vals;
+  const Bucket* idx;
   uint64_t mask;
   const int64_t* e_off;
   const int32_t* e_len;
@@ -651,7 +675,7 @@ template <bool CLOSEST, int STACK>
 __global__ void __launch_bounds__(128) k_predict(PredictArgs a) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  int32_t e = a.idx_keys ? index_lookup(a.idx_keys, a.idx_vals, a.mask, a.keys[i]) : -1;
+  int32_t e = a.idx ? index_lookup(a.idx, a.mask, a.keys[i]) : -1;
   Hit acc = empty_entry_result(CLOSEST);
   int8_t c = 2;
   if (e >= 0) {
@@ -686,7 +710,7 @@ int predict_batch(const BvhDev& b, TableDev& t, const uint64_t* keys, const floa
                   int8_t* cls, double* tt, int32_t* slot, int32_t* leaf, double* u, double* v,
                   int64_t* box, int64_t* tri, int64_t* vis, int64_t* est, cudaStream_t st) {
   if (n <= 0) return 0;
-  PredictArgs a{b.nodes, b.tris, b.depth, t.n_entries ? t.idx_keys : nullptr, t.idx_vals,
+  PredictArgs a{b.nodes, b.tris, b.depth, t.n_entries ? t.idx : nullptr,
                 (uint64_t)t.idx_cap - 1, t.e_off, t.e_len, t.arena, keys, O, D, tmin, tmax, n,
                 cls, tt, slot, leaf, u, v, box, tri, vis, est};
   int grid = (int)((n + 127) / 128);
