@@ -37,6 +37,9 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "Mrays/s with HRPP prediction vs full traversal; % BVH node visits skipped"
 KINDS = ("primary", "shadow", "bounce")
+STATS_NAMES = ("rays", "tp", "fp", "neg", "baseline_box_tests", "baseline_tri_tests",
+               "overhead_box_tests", "overhead_tri_tests", "skipped_box_tests",
+               "skipped_box_tests_estimated", "wrong_closest")
 
 
 def parse():
@@ -373,6 +376,8 @@ def run_ours(args, rank, world, local_rank):
             "speedup_vs_full_traversal": round(value / base_value, 4),
             "nodes_skipped_percent": savings,
             "live_node_visit_reduction_percent": round(visit_reduction, 3),
+            "limit_stats": {k: dict(zip(STATS_NAMES, map(int, lim_stats[k]))) for k in KINDS},
+            "live_stats": {k: dict(zip(STATS_NAMES, map(int, live_stats[k]))) for k in KINDS},
             "stages": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }

@@ -50,6 +50,7 @@ def _load():
     L.hrpp_device_count.argtypes = [P]
     L.hrpp_set_live_rounds.argtypes = [C.c_int]
     L.hrpp_set_consult_short.argtypes = [C.c_int]
+    L.hrpp_set_trace_persistent.argtypes = [C.c_int]
     L.hrpp_profile_enable.argtypes = [C.c_int]
     L.hrpp_profile_read.argtypes = [P, P, C.c_int, C.c_int]
     L.hrpp_hash_rays.argtypes = [P, P, I64, C.c_int, P, P]
@@ -78,7 +79,8 @@ def _load():
                  "hrpp_table_info", "hrpp_table_record", "hrpp_table_lookup",
                  "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
                  "hrpp_profile_enable", "hrpp_profile_read", "hrpp_table_set_deferred",
-                 "hrpp_table_pending", "hrpp_set_consult_short"):
+                 "hrpp_table_pending", "hrpp_set_consult_short",
+                 "hrpp_set_trace_persistent"):
         getattr(L, name).restype = C.c_int
     return L
 
@@ -104,7 +106,8 @@ EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device
             "hrpp_table_destroy", "hrpp_table_clear", "hrpp_table_info", "hrpp_table_record",
             "hrpp_table_lookup", "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
             "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
-            "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short")
+            "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short",
+            "hrpp_set_trace_persistent")
 
 PROFILE_STAGES = ("hash", "trace", "trace_queue", "group", "consult", "commit", "other")
 

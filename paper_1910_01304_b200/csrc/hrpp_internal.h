@@ -138,6 +138,7 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
 int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, int* count_dev,
                   cudaStream_t st);
 extern int g_consult_short;
+extern int g_trace_persistent;
 // values[i] for i < n with flags[i] != 0, in order, count to *count_dev
 int compact_by_flags(Workspace& ws, const int32_t* values, const uint8_t* flags, int64_t n,
                      int32_t* out, int* count_dev, cudaStream_t st);

@@ -25,6 +25,8 @@
 // unknown, the queue is traced and the replay resumes; after `rounds` exact
 // rounds one speculative round traces every unresolved ray.  Either way the
 // results are exact: speculation only costs traversals.
+#include <cub/cub.cuh>
+
 #include "hrpp_internal.h"
 
 namespace hrpp {
@@ -477,30 +479,123 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
   }
 }
 
-// Thread t owns key segment t; segments longer than `short_len` rays are
-// replayed cooperatively by the owning warp.
+// Short segments: thread t owns key segment t.
 template <bool CLOSEST, bool LIVE, int STACK>
-__global__ void __launch_bounds__(128) k_replay(ConsultArgs a, int short_len) {
+__global__ void __launch_bounds__(128) k_replay_short(ConsultArgs a, int short_len) {
   if (*a.err) return;
-  const int lane = threadIdx.x & 31;
   const int ns = *a.nsegs;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   Tally c;
-  bool active = false, small = false;
-  int32_t beg = 0, end = 0, cur = 0;
   if (s < ns) {
+    const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
+    const int32_t cur = a.seg_cursor[s];
+    if (cur < end && end - beg <= short_len) seg_thread<CLOSEST, LIVE, STACK>(a, c, s, beg, end, cur);
+  }
+  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
+  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 10; k++) {
+    long long w = warp_sum(v[k]);
+    if (lane == 0 && w) atomicAdd(a.stats + slot[k], (unsigned long long)w);
+  }
+}
+
+// Long segments: one warp per segment of the compacted list.
+template <bool CLOSEST, bool LIVE, int STACK>
+__global__ void __launch_bounds__(128) k_replay_long(ConsultArgs a, const int32_t* list,
+                                                     const int* count) {
+  if (*a.err) return;
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int m = *count;
+  Tally c;
+  for (int k = w; k < m; k += nw) seg_warp<CLOSEST, LIVE, STACK>(a, c, list[k], lane);
+  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
+  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
+#pragma unroll
+  for (int k = 0; k < 10; k++) {
+    long long x = warp_sum(v[k]);
+    if (lane == 0 && x) atomicAdd(a.stats + slot[k], (unsigned long long)x);
+  }
+}
+
+// Grouped single-tile replay: a group of G lanes replays one key segment
+// with at most G rays left (the rays after its first append), 32/G segments
+// per warp.  Within a group this is seg_warp's ballot loop.
+template <bool CLOSEST, bool LIVE, int STACK, int G>
+__global__ void __launch_bounds__(128) k_replay_group(ConsultArgs a, const int32_t* list,
+                                                      int count) {
+  if (*a.err) return;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G, gbase = lane - gl;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+  const int gid = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  Tally c;
+  const bool gvalid = gid < count;
+  int s = 0;
+  int32_t beg = 0, end = 0, tb = 0, napp = 0, ex_len = 0;
+  int64_t ex_off = 0;
+  if (gvalid) {
+    s = list[gid];
     beg = a.seg_start[s];
     end = a.seg_start[s + 1];
-    cur = a.seg_cursor[s];
-    active = cur < end;
-    small = end - beg <= short_len;
+    tb = a.seg_cursor[s];
+    napp = a.seg_napp[s];
+    ex_off = a.seg_exoff[s];
+    ex_len = a.seg_exlen[s];
   }
-  if (active && small) seg_thread<CLOSEST, LIVE, STACK>(a, c, s, beg, end, cur);
-  unsigned lm = __ballot_sync(kFull, active && !small);
-  while (lm) {
-    const int l = __ffs(lm) - 1;
-    lm &= lm - 1;
-    seg_warp<CLOSEST, LIVE, STACK>(a, c, __shfl_sync(kFull, s, l), lane);
+  int32_t* app = a.app + beg;
+  const int32_t pos = tb + gl;
+  const bool valid = gvalid && pos < end;
+  const int32_t idx = valid ? a.sidx[pos] : 0;
+  Hit acc = empty_entry_result(CLOSEST);
+  int32_t applied = 0;
+  if (valid) load_state(a, idx, acc, applied);
+  int32_t L = ex_len + napp;
+  int32_t cnode = -1;
+  if (valid && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
+  bool inL = false;
+  if (valid)
+    for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
+  Ray r{};
+  if (valid) {
+    r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+    if (applied < L && (CLOSEST || !acc.found))
+      catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+  }
+  int cur_l = 0;
+  for (;;) {
+    const bool need = valid && gl >= cur_l && (L == 0 || !acc.found);
+    const unsigned m = __ballot_sync(kFull, need) & gmask;
+    const int f = m ? __ffs(m) - 1 - gbase : G;
+    if (valid && gl >= cur_l && gl < f) commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+    if (!__any_sync(kFull, f < G)) break;
+    const int src = f < G ? gbase + f : lane;
+    const int32_t cf = __shfl_sync(kFull, cnode, src);
+    const bool inLf = __shfl_sync(kFull, inL, src);
+    const int32_t rf = __shfl_sync(kFull, idx, src);
+    const bool grow = f < G && cf >= 0 && !inLf;
+    if (f < G && gl == f) commit_miss<LIVE>(a, c, idx, acc, L == 0);
+    if (grow && gl == 0) {  // record(key, anc[leaf]) grows the entry
+      app[napp] = cf;
+      a.app_ray[beg + napp] = rf;
+    }
+    __syncwarp();
+    if (grow) {
+      napp++;
+      L++;
+      inL |= cnode == cf;
+      if (valid && gl > f && (CLOSEST || !acc.found))
+        catch_up<CLOSEST, STACK>(a, r, acc, L - 1, L, ex_off, ex_len, app);
+    }
+    if (f < G) cur_l = f + 1;
+    else cur_l = G;
+  }
+  if (gvalid && gl == 0) {
+    a.seg_napp[s] = napp;
+    a.seg_cursor[s] = end;
   }
   long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
   const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
@@ -508,6 +603,50 @@ __global__ void __launch_bounds__(128) k_replay(ConsultArgs a, int short_len) {
   for (int k = 0; k < 10; k++) {
     long long w = warp_sum(v[k]);
     if (lane == 0 && w) atomicAdd(a.stats + slot[k], (unsigned long long)w);
+  }
+}
+
+// Replay length class of every segment (rays left): 0 done, 1..6 for
+// <= 1, 2, 4, 8, 16, 32 rays, 7 longer.
+__global__ void k_replay_class(ConsultArgs a, int64_t nseg_cap, uint8_t* cls, int32_t* ids) {
+  const int ns = *a.nsegs;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg_cap;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    if (s < ns) {
+      const int32_t rem = a.seg_start[s + 1] - a.seg_cursor[s];
+      k = rem <= 0 ? 0 : rem <= 1 ? 1 : rem <= 2 ? 2 : rem <= 4 ? 3 : rem <= 8 ? 4
+        : rem <= 16 ? 5 : rem <= 32 ? 6 : 7;
+    }
+    cls[s] = (uint8_t)k;
+    ids[s] = (int32_t)s;
+  }
+}
+
+// Start of every class in the class-sorted list (8 entries + end).
+__global__ void k_class_bounds(const uint8_t* sorted_cls, int64_t m, int* bounds) {
+  const int k = threadIdx.x;
+  if (k > 8) return;
+  int64_t lo = 0, hi = m;  // first position with class >= k
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (sorted_cls[mid] < k) lo = mid + 1;
+    else hi = mid;
+  }
+  bounds[k] = (int)lo;
+}
+
+// Flags of the active segments longer than short_len.
+__global__ void k_long_flags(ConsultArgs a, int64_t n, int short_len, uint8_t* flags) {
+  const int ns = *a.nsegs;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    bool f = false;
+    if (s < ns) {
+      const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
+      f = a.seg_cursor[s] < end && end - beg > short_len;
+    }
+    flags[s] = f;
   }
 }
 
@@ -522,26 +661,124 @@ __global__ void k_check_done(const int* nsegs, const int32_t* seg_start,
 // host orchestration
 // ---------------------------------------------------------------------------
 
-template <bool CLOSEST, bool LIVE>
-static void dispatch_replay(int stack, int grid, cudaStream_t st, const ConsultArgs& a) {
+struct LongList {
+  uint8_t* flags;
+  int32_t* list;
+  int* count;
+  int64_t nsegs_host;  // upper bound on the number of segments
+};
+
+template <bool CLOSEST, bool LIVE, int STACK>
+static int replay_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, const LongList& L,
+                       int64_t n) {
   const int sl = g_consult_short;
+  const int grid_s = (int)((L.nsegs_host + 127) / 128);
+  k_replay_short<CLOSEST, LIVE, STACK><<<grid_s > 0 ? grid_s : 1, 128, 0, st>>>(a, sl);
+  HRPP_LAUNCHED();
+  k_long_flags<<<grid_for(L.nsegs_host, 256, num_sms() * 8), 256, 0, st>>>(a, L.nsegs_host, sl,
+                                                                           L.flags);
+  HRPP_LAUNCHED();
+  int rc;
+  if ((rc = compact_flags(ws, L.flags, L.nsegs_host, L.list, L.count, st))) return rc;
+  // one warp per long segment (at most nsegs / (short_len + 1) of them)
+  int64_t max_long = L.nsegs_host / (sl + 1) + 1;
+  if (max_long > L.nsegs_host) max_long = L.nsegs_host;
+  const int grid_l = (int)((max_long * 32 + 127) / 128);
+  k_replay_long<CLOSEST, LIVE, STACK><<<grid_l > 0 ? grid_l : 1, 128, 0, st>>>(a, L.list, L.count);
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+template <bool CLOSEST, bool LIVE>
+static int dispatch_replay(int stack, cudaStream_t st, const ConsultArgs& a, Workspace& ws,
+                           const LongList& L, int64_t n) {
   switch (stack) {
-    case 64: k_replay<CLOSEST, LIVE, 64><<<grid, 128, 0, st>>>(a, sl); break;
-    case 256: k_replay<CLOSEST, LIVE, 256><<<grid, 128, 0, st>>>(a, sl); break;
-    default: k_replay<CLOSEST, LIVE, 512><<<grid, 128, 0, st>>>(a, sl); break;
+    case 64: return replay_impl<CLOSEST, LIVE, 64>(st, a, ws, L, n);
+    case 256: return replay_impl<CLOSEST, LIVE, 256>(st, a, ws, L, n);
+    default: return replay_impl<CLOSEST, LIVE, 512>(st, a, ws, L, n);
   }
 }
 
-static void launch_replay(bool closest, bool live, int stack, int grid, cudaStream_t st,
-                          const ConsultArgs& a) {
+static int launch_replay(bool closest, bool live, int stack, cudaStream_t st,
+                         const ConsultArgs& a, Workspace& ws, const LongList& L, int64_t n) {
   ProfScope ps(P_CONSULT, st);
-  if (closest) {
-    if (live) dispatch_replay<true, true>(stack, grid, st, a);
-    else dispatch_replay<true, false>(stack, grid, st, a);
-  } else {
-    if (live) dispatch_replay<false, true>(stack, grid, st, a);
-    else dispatch_replay<false, false>(stack, grid, st, a);
+  if (closest)
+    return live ? dispatch_replay<true, true>(stack, st, a, ws, L, n)
+                : dispatch_replay<true, false>(stack, st, a, ws, L, n);
+  return live ? dispatch_replay<false, true>(stack, st, a, ws, L, n)
+              : dispatch_replay<false, false>(stack, st, a, ws, L, n);
+}
+
+// All full results known: replay every length class with its own group size.
+template <bool CLOSEST, bool LIVE, int STACK>
+static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, int64_t nseg_cap) {
+  uint8_t *cls, *cls_sorted;
+  int32_t *ids, *ids_sorted;
+  int* bounds;
+  int rc;
+  const int64_t m = nseg_cap > 0 ? nseg_cap : 1;
+  if ((rc = ws.get("rg_cls", m, &cls)) || (rc = ws.get("rg_cls2", m, &cls_sorted)) ||
+      (rc = ws.get("rg_ids", m, &ids)) || (rc = ws.get("rg_ids2", m, &ids_sorted)) ||
+      (rc = ws.get("rg_bounds", 16, &bounds)))
+    return rc;
+  k_replay_class<<<grid_for(m, 256, num_sms() * 8), 256, 0, st>>>(a, m, cls, ids);
+  HRPP_LAUNCHED();
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 3, st);
+  void* tmp;
+  if ((rc = ws.get_raw("rg_tmp", b, &tmp))) return rc;
+  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 3,
+                                          st));
+  k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds);
+  HRPP_LAUNCHED();
+  int hb[9];
+  HRPP_CK(cudaMemcpyAsync(hb, bounds, sizeof(int) * 9, cudaMemcpyDeviceToHost, st));
+  HRPP_CK(cudaStreamSynchronize(st));
+  auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
+#define HRPP_GROUP(K, GS)                                                                      \
+  if (cnt(K) > 0) {                                                                            \
+    const int64_t thr = (int64_t)cnt(K) * GS;                                                  \
+    k_replay_group<CLOSEST, LIVE, STACK, GS><<<(int)((thr + 127) / 128), 128, 0, st>>>(       \
+        a, ids_sorted + hb[K], cnt(K));                                                        \
+    HRPP_LAUNCHED();                                                                           \
   }
+  HRPP_GROUP(1, 1)
+  HRPP_GROUP(2, 2)
+  HRPP_GROUP(3, 4)
+  HRPP_GROUP(4, 8)
+  HRPP_GROUP(5, 16)
+  HRPP_GROUP(6, 32)
+#undef HRPP_GROUP
+  if (cnt(7) > 0) {
+    int* dcount;
+    if ((rc = ws.get("rg_lcount", 1, &dcount))) return rc;
+    const int c7 = cnt(7);
+    HRPP_CK(cudaMemcpyAsync(dcount, &c7, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_replay_long<CLOSEST, LIVE, STACK><<<(c7 * 32 + 127) / 128, 128, 0, st>>>(
+        a, ids_sorted + hb[7], dcount);
+    HRPP_LAUNCHED();
+  }
+  return 0;
+}
+
+template <bool CLOSEST, bool LIVE>
+static int dispatch_grouped(int stack, cudaStream_t st, const ConsultArgs& a, Workspace& ws,
+                            int64_t nseg_cap) {
+  switch (stack) {
+    case 64: return grouped_impl<CLOSEST, LIVE, 64>(st, a, ws, nseg_cap);
+    case 256: return grouped_impl<CLOSEST, LIVE, 256>(st, a, ws, nseg_cap);
+    default: return grouped_impl<CLOSEST, LIVE, 512>(st, a, ws, nseg_cap);
+  }
+}
+
+static int launch_grouped(bool closest, bool live, int stack, cudaStream_t st,
+                          const ConsultArgs& a, Workspace& ws, int64_t nseg_cap) {
+  ProfScope ps(P_CONSULT, st);
+  if (closest)
+    return live ? dispatch_grouped<true, true>(stack, st, a, ws, nseg_cap)
+                : dispatch_grouped<true, false>(stack, st, a, ws, nseg_cap);
+  return live ? dispatch_grouped<false, true>(stack, st, a, ws, nseg_cap)
+              : dispatch_grouped<false, false>(stack, st, a, ws, nseg_cap);
 }
 
 template <bool CLOSEST>
@@ -616,7 +853,12 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       (rc = ws.get("k_f1", n, &a.seg_f1)) || (rc = ws.get("k_segofray", n, &a.seg_of_ray)) ||
       (rc = ws.get("k_posofray", n, &a.pos_of_ray)))
     return rc;
-  const int grid = (int)((n + 127) / 128);  // thread t owns segment t (nsegs <= n)
+  const int grid = (int)((n + 127) / 128);
+  LongList LL;
+  LL.nsegs_host = nsegs_h;
+  if ((rc = ws.get("k_lflags", nsegs_h + 1, &LL.flags)) || (rc = ws.get("k_llist", nsegs_h + 1, &LL.list)) ||
+      (rc = ws.get("k_lcount", 1, &LL.count)))
+    return rc;
   {
     ProfScope ps(P_CONSULT, st);
     k_seg_lookup<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a, n);
@@ -671,8 +913,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       if (rounds > 0) {
         a.spec = r == rounds ? 2 : 0;
         HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
-        launch_replay(t.closest, true, b.stack, grid, st, a);
-        HRPP_LAUNCHED();
+        if ((rc = launch_replay(t.closest, true, b.stack, st, a, ws, LL, n))) return rc;
       }
       // the rays whose full traversal is needed next, compacted in ray order:
       // neighbouring pixels share warps in the traversal kernel (key order
@@ -685,9 +926,10 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.spec = 0;
     if (rounds == 0) {
       if ((rc = finalize_prefix(t.closest, true, grid, st, a, n))) return rc;
+      if ((rc = launch_grouped(t.closest, true, b.stack, st, a, ws, nsegs_h))) return rc;
+    } else {
+      if ((rc = launch_replay(t.closest, true, b.stack, st, a, ws, LL, n))) return rc;
     }
-    launch_replay(t.closest, true, b.stack, grid, st, a);
-    HRPP_LAUNCHED();
     k_check_done<<<grid_for(n, 256, num_sms() * 4), 256, 0, st>>>(seg.nsegs, seg.seg_start,
                                                                  a.seg_cursor, err);
     HRPP_LAUNCHED();
@@ -707,8 +949,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       HRPP_LAUNCHED();
     }
     if ((rc = finalize_prefix(t.closest, false, grid, st, a, n))) return rc;
-    launch_replay(t.closest, false, b.stack, grid, st, a);
-    HRPP_LAUNCHED();
+    if ((rc = launch_grouped(t.closest, false, b.stack, st, a, ws, nsegs_h))) return rc;
   }
   if (t.deferred)
     return table_collect_pending(t, seg, n, a.seg_napp, a.app, a.app_ray, err, st);

@@ -164,6 +164,163 @@ __global__ void __launch_bounds__(128) k_trace(TraceArgs a) {
   }
 }
 
+// Persistent traversal for divergent (secondary) waves: warps stay resident
+// and refill finished lanes from a per-warp chunk of rays (one global atomic
+// per 256 rays) whenever fewer than kRefillBelow lanes are busy.  Each ray's
+// node-visit sequence is exactly trace_from's, so results are identical.
+constexpr int kChunk = 256;
+#ifndef HRPP_REFILL_BELOW
+#define HRPP_REFILL_BELOW 24
+#endif
+#ifndef HRPP_PERSIST_STEPS
+#define HRPP_PERSIST_STEPS 16
+#endif
+constexpr int kRefillBelow = HRPP_REFILL_BELOW;
+int g_trace_persistent = 0;
+
+template <bool CLOSEST>
+__device__ __forceinline__ void store_hit(const TraceOut& o, int64_t i, const Hit& h) {
+  if (o.found) o.found[i] = h.found;
+  if (o.t) o.t[i] = h.t;
+  if (o.slot) o.slot[i] = h.slot;
+  if (o.leaf) o.leaf[i] = h.leaf;
+  if (CLOSEST && o.u) o.u[i] = h.u;
+  if (CLOSEST && o.v) o.v[i] = h.v;
+  if (o.box) o.box[i] = h.boxes;
+  if (o.tri) o.tri[i] = h.tris;
+  if (o.vis) o.vis[i] = h.boxes;
+  if (o.known) o.known[i] = 1;
+}
+
+template <bool CLOSEST, int STACK>
+__global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_counter) {
+  if (a.err && *a.err) return;
+  const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.n;
+  const int lane = threadIdx.x & 31;
+  int32_t stack[STACK];
+  int top = 0;
+  Hit h;
+  h.found = false; h.t = 0.0; h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0;
+  h.boxes = 0; h.tris = 0;
+  Ray r{};
+  int64_t cur = -1;
+  int64_t c_lo = 0, c_hi = 0;
+  bool more = true;
+  unsigned long long sb = 0, stt = 0;
+  for (;;) {
+    unsigned busy = __ballot_sync(0xffffffffu, cur >= 0);
+    if (more && __popc(busy) < kRefillBelow) {
+      unsigned idle = ~busy;
+      while (idle && more) {
+        if (c_lo >= c_hi) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(chunk_counter, kChunk);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          c_lo = base;
+          c_hi = (int64_t)base + kChunk < count ? (int64_t)base + kChunk : count;
+          if (c_lo >= count) {
+            more = false;
+            break;
+          }
+        }
+        const int avail = (int)(c_hi - c_lo);
+        const int rank = __popc(idle & ((1u << lane) - 1u));
+        if (cur < 0 && rank < avail) {
+          const int64_t q = c_lo + rank;
+          cur = a.ray_idx ? (int64_t)a.ray_idx[q] : q;
+          r = make_ray(a.O, a.D, a.tmin, a.tmax, cur);
+          stack[0] = a.start;
+          top = 1;
+          h.found = false;
+          h.t = CLOSEST ? r.tmax : 0.0;
+          h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0; h.boxes = 0; h.tris = 0;
+        }
+        const int took = __popc(idle) < avail ? __popc(idle) : avail;
+        c_lo += took;
+        idle = __ballot_sync(0xffffffffu, cur < 0);
+      }
+      busy = __ballot_sync(0xffffffffu, cur >= 0);
+    }
+    if (!busy) break;
+    if (cur >= 0) {
+      // up to kStepsPerRefill node visits of trace_from (hrpp/kernels.py:112-153)
+      for (int it = 0; it < HRPP_PERSIST_STEPS && top > 0; it++) {
+        const int32_t nd = stack[--top];
+        h.boxes++;
+        float4 lo, hi;
+        load_node(a.nodes, nd, lo, hi);
+        if (!box_hit(lo, hi, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin,
+                     CLOSEST ? h.t : r.tmax))
+          continue;
+        const int32_t na = __float_as_int(lo.w);
+        const int32_t nb = __float_as_int(hi.w);
+        if (na < 0) {
+          const int32_t f = ~na, e = f + nb;
+          for (int32_t k = f; k < e; k++) {
+            double t, u, v;
+            h.tris++;
+            if (tri_test(a.tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) &&
+                t >= r.tmin && t <= r.tmax) {
+              if (!CLOSEST || !h.found || t < h.t) {
+                h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+              }
+              if (!CLOSEST) {
+                top = 0;
+                break;
+              }
+            }
+          }
+        } else {
+          const int axis = (uint32_t)nb >> 30;
+          const int32_t right = nb & 0x3FFFFFFF;
+          const double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
+          stack[top++] = dval >= 0.0 ? right : na;
+          stack[top++] = dval >= 0.0 ? na : right;
+        }
+      }
+      if (top == 0) {
+        store_hit<CLOSEST>(a.out, cur, h);
+        sb += h.boxes;
+        stt += h.tris;
+        cur = -1;
+      }
+    }
+  }
+  if (a.out.sums) {
+    sb = warp_sum(sb);
+    stt = warp_sum(stt);
+    if (lane == 0 && (sb | stt)) {
+      atomicAdd(a.out.sums, sb);
+      atomicAdd(a.out.sums + 1, stt);
+    }
+  }
+}
+
+template <bool CLOSEST, int STACK>
+static void launch_persist(cudaStream_t st, const TraceArgs& a, int* counter) {
+  static int per_sm = 0;  // resident blocks of this instantiation
+  if (!per_sm &&
+      (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_persist<CLOSEST, STACK>,
+                                                     128, 0) != cudaSuccess ||
+       per_sm < 1))
+    per_sm = 4;
+  const int64_t need = (a.n + 127) / 128;
+  const int64_t res = (int64_t)num_sms() * per_sm;
+  const int grid = (int)(res < need ? res : (need > 0 ? need : 1));
+  k_trace_persist<CLOSEST, STACK><<<grid, 128, 0, st>>>(a, counter);
+}
+
+template <bool CLOSEST>
+static void dispatch_persist(int stack, cudaStream_t st, const TraceArgs& a, int* counter) {
+  switch (stack) {
+    case 32: launch_persist<CLOSEST, 32>(st, a, counter); break;
+    case 64: launch_persist<CLOSEST, 64>(st, a, counter); break;
+    case 128: launch_persist<CLOSEST, 128>(st, a, counter); break;
+    case 256: launch_persist<CLOSEST, 256>(st, a, counter); break;
+    default: launch_persist<CLOSEST, 512>(st, a, counter); break;
+  }
+}
+
 template <bool CLOSEST>
 static void dispatch_trace(int stack, int grid, cudaStream_t st, const TraceArgs& a) {
   switch (stack) {
@@ -181,10 +338,21 @@ int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const int* err, cudaStream_t st) {
   if (n <= 0) return 0;
   TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
-  int grid = (int)((n + 127) / 128);
   ProfScope ps(ray_idx ? P_TRACE_QUEUE : P_TRACE, st);
-  if (closest) dispatch_trace<true>(b.stack, grid, st, a);
-  else dispatch_trace<false>(b.stack, grid, st, a);
+  if (g_trace_persistent) {
+    static int* counters[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int*& counter = counters[dev & 63];
+    if (!counter) HRPP_CK(cudaMalloc(&counter, sizeof(int)));
+    HRPP_CK(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    if (closest) dispatch_persist<true>(b.stack, st, a, counter);
+    else dispatch_persist<false>(b.stack, st, a, counter);
+  } else {
+    int grid = (int)((n + 127) / 128);
+    if (closest) dispatch_trace<true>(b.stack, grid, st, a);
+    else dispatch_trace<false>(b.stack, grid, st, a);
+  }
   HRPP_LAUNCHED();
   return 0;
 }

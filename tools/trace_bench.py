@@ -23,7 +23,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--res", default=None)
+    ap.add_argument("--persistent", type=int, default=1)
     a = ap.parse_args()
+    hb._lib.lib.hrpp_set_trace_persistent(a.persistent)
     res = tuple(int(x) for x in a.res.split("x")) if a.res else None
     sc = scenes.make_scene(a.config, resolution=res)
     b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
@@ -40,6 +42,8 @@ def main():
           else np.broadcast_to(np.asarray(sc.point_lights[0]), P.shape))
     so, sd, s0, s1 = scenes.shadow_rays(P, lp)
     S = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (so, sd, s0, s1)]
+    bo, bd, b0, b1 = scenes.cosine_bounce(P, N, seed=0)
+    B = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (bo, bd, b0, b1)]
 
     def timeit(fn):
         for _ in range(3):
@@ -56,8 +60,10 @@ def main():
 
     ms_c = timeit(lambda: hb.intersect_closest_batch(b, Ot, Dt, t0, t1))
     ms_a = timeit(lambda: hb.intersect_any_batch(b, *S))
+    ms_b = timeit(lambda: hb.intersect_closest_batch(b, *B))
     print(json.dumps({"closest_ms": round(ms_c, 4), "closest_mrays_s": round(n / ms_c / 1e3, 1),
                       "any_ms": round(ms_a, 4), "any_mrays_s": round(len(so) / ms_a / 1e3, 1),
+                      "bounce_ms": round(ms_b, 4), "bounce_mrays_s": round(len(bo) / ms_b / 1e3, 1),
                       "mean_box": float(base["box"].mean()), "n": n}))
 
 
