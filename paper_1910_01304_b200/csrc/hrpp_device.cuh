@@ -127,9 +127,12 @@ template <bool CLOSEST, int STACK>
 __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
                                           const DTri* __restrict__ tris, const Ray& r,
                                           int32_t start) {
+  // The reference pushes far then near and pops near next; visiting the near
+  // child directly (only far goes to the stack) is the same visit order with
+  // one local-memory store and load less per interior node.
   int32_t stack[STACK];
-  int top = 1;
-  stack[0] = start;
+  int top = 0;
+  int32_t nd = start;
   Hit h;
   h.found = false;
   h.t = CLOSEST ? r.tmax : 0.0;
@@ -139,17 +142,22 @@ __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
   h.v = 0.0;
   h.boxes = 0;
   h.tris = 0;
-  while (top > 0) {
-    int32_t nd = stack[--top];
+  for (;;) {
     h.boxes++;
     float4 lo, hi;
     load_node(nodes, nd, lo, hi);
-    if (!box_hit(lo, hi, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax))
-      continue;
-    int32_t a = __float_as_int(lo.w);
-    int32_t b = __float_as_int(hi.w);
-    if (a < 0) {
-      int32_t f = ~a, e = f + b;
+    if (box_hit(lo, hi, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax)) {
+      const int32_t a = __float_as_int(lo.w);
+      const int32_t b = __float_as_int(hi.w);
+      if (a >= 0) {
+        const int axis = (uint32_t)b >> 30;
+        const int32_t right = b & 0x3FFFFFFF;
+        const double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
+        stack[top++] = dval >= 0.0 ? right : a;  // far
+        nd = dval >= 0.0 ? a : right;            // near, visited next
+        continue;
+      }
+      const int32_t f = ~a, e = f + b;
       for (int32_t k = f; k < e; k++) {
         double t, u, v;
         h.tris++;
@@ -164,15 +172,9 @@ __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
           }
         }
       }
-    } else {
-      int axis = (uint32_t)b >> 30;
-      int32_t right = b & 0x3FFFFFFF;
-      double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
-      int32_t nearc = dval >= 0.0 ? a : right;
-      int32_t farc = dval >= 0.0 ? right : a;
-      stack[top++] = farc;
-      stack[top++] = nearc;
     }
+    if (top == 0) break;
+    nd = stack[--top];
   }
   return h;
 }
