@@ -121,6 +121,27 @@ int hrpp_build_bvh(const float *v0, const float *v1, const float *v2, const int3
                    float *tv2, int32_t *tri_ids, int64_t *n_nodes_out, int64_t *n_tris_out,
                    int32_t *max_depth_out);
 
+/* ---- ray generation and spawning on the device (waves stay in HBM) ----- */
+/* generate_primary_rays (hrpp/tracer.py:173-211) with unit_floats
+ * (hrpp/rng.py:23-31): O, D device (width*height*spp, 3) float32, pixel-major /
+ * sample-minor; basis9 = camera (forward, right, up) float64 from
+ * Camera.basis (hrpp/tracer.py:84-97); sx, sy = the stratum grid. */
+int hrpp_gen_primary(const float *cam_pos, const double *basis9, double tan_half, double aspect,
+                     int64_t width, int64_t height, int64_t spp, int64_t sx, int64_t sy,
+                     uint64_t seed, int jitter, float *O, float *D, void *stream);
+/* Secondary waves from a closest-hit wave's hits (device arrays): hit points
+ * offset 1e-4 along the facing geometric normal (hrpp/tracer.py:442-453).
+ * shadow_kind 1 = point light light3 (hrpp/tracer.py:456-464), 2 = y-facing
+ * square area light centred at light3 with half extent `half` (uniform
+ * samples); bounce_kind 1 = mirror (hrpp/tracer.py:488-492), 2 =
+ * cosine-weighted diffuse.  Outputs sized n (hits are compacted in ray
+ * order); *count_out = number of hits. */
+int hrpp_spawn(hrpp_bvh_t bvh, const float *O, const float *D, const uint8_t *found,
+               const double *t, const int32_t *slot, int64_t n, int shadow_kind,
+               const double *light3, double half, int bounce_kind, uint64_t seed, float *so,
+               float *sd, double *s0, double *s1, float *bo, float *bd, double *b0, double *b1,
+               int64_t *count_out, void *stream);
+
 /* ---- traversal batch: hrpp/kernels.py:209-248 via hrpp/bvh.py:398-442 --- */
 /* kind = HRPP_CLOSEST_HIT or HRPP_HIT_ANY; start = subtree root (0 = root).
  * out->u/v ignored for hit-any (the reference batch has none). */

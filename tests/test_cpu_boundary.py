@@ -141,3 +141,23 @@ def test_scene_sizes():
         assert icosphere(s)[1].shape[0] == f
     c1 = make_scene("c1")
     assert c1.n_tris == 1282
+
+
+def test_report_rows_match_reference_format(tmp_path):
+    s = hb.RayKindStats(rays=10, tp=3, fp=2, neg=5, baseline_box_tests=50, baseline_tri_tests=9,
+                        overhead_box_tests=4, overhead_tri_tests=3, skipped_box_tests=20)
+    ts = hb.TableStats(entries=1, stored_nodes=1, avg_nodes_per_entry=1.0,
+                       max_nodes_per_entry=1,
+                       memory=hb.MemoryEstimate(entry_bytes=16, node_ref_bytes=4))
+    row = hb.report_row("demo", "limit", "primary", 6, 0, 8, "64x64", 0, s, ts)
+    assert set(hb.REPORT_COLUMNS) == set(row)
+    assert row["savings_percent"] == pytest.approx(40.0) and row["consulted"] == 10
+    text = hb.render_csv([row], timestamp=False)
+    assert text.splitlines()[0] == ",".join(hb.REPORT_COLUMNS)
+    assert "40.000000" in text.splitlines()[1]
+    assert hb.render_csv([row]).startswith("# generated ")
+    hb.write_json([row], tmp_path / "r.json")
+    import json
+    assert json.loads((tmp_path / "r.json").read_text())[0]["tp"] == 3
+    f = hb.failed_row("demo", "limit", "primary", 6, 0, 8, "64x64", 0, "boom")
+    assert f["status"] == "failed: boom" and f["rays"] == 0

@@ -480,3 +480,62 @@ def test_consult_paths_identical(hb, short, mode):
         assert list(t.dump_lines()) == list(ref["primary_dump"])
     finally:
         hb.set_consult_short(32)
+
+
+# -- ray generation and spawning on the device --------------------------------------------
+
+def test_gpu_primary_rays_bit_exact(hb):
+    from paper_1910_01304_b200.scenes import Camera
+    from paper_1910_01304_b200.waves import generate_primary_rays
+    g = load_golden("wave_inputs.npz")
+    cam = Camera((7.0, 5.5, 9.5), (0.0, 0.6, 0.0), (0.0, 1.0, 0.0), 42.0, (48, 48))
+    O, D = generate_primary_rays(cam, 4, seed=0, to_host=True)
+    assert np.array_equal(O, g["primary_O"]) and np.array_equal(D, g["primary_D"])
+    # a larger, unjittered and odd-spp case against the numpy generator
+    from paper_1910_01304_b200 import scenes
+    cam2 = Camera((0.0, 0.3, 3.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 60.0, (257, 129))
+    for spp, jit in ((3, True), (8, False)):
+        O2, D2 = generate_primary_rays(cam2, spp, seed=5, jitter=jit, to_host=True)
+        R2 = scenes.primary_rays(cam2, spp, seed=5, jitter=jit)
+        assert np.array_equal(O2, R2[0]) and np.array_equal(D2, R2[1])
+
+
+def test_gpu_spawn_matches_reference_renderer(hb):
+    """Point-light shadows and mirror bounces equal the reference renderer's
+    numpy spawn (tests/golden/make_golden.py spawn_shadow) bit for bit."""
+    from paper_1910_01304_b200.waves import spawn_secondary
+    g = load_golden("wave_inputs.npz")
+    b = gbvh(hb, "spheres")
+    O, D = g["primary_O"], g["primary_D"]
+    n = O.shape[0]
+    base = hb.intersect_closest_batch(b, O, D, np.zeros(n), np.full(n, np.inf))
+    light = (8.0, 10.0, 6.0)  # bundled spheres scene, light 0
+    w = spawn_secondary(b, O, D, base, shadow=("point", light), bounce="mirror")
+    so, sd, s0, s1 = (x.cpu().numpy() for x in w["shadow"])
+    assert np.array_equal(so, g["shadow_O"]) and np.array_equal(sd, g["shadow_D"])
+    assert np.array_equal(s1, g["shadow_tmax"]) and np.array_equal(s0, g["shadow_tmin"])
+    bo, bd, _, b1 = (x.cpu().numpy() for x in w["bounce"])
+    assert np.array_equal(bo, g["reflection_O"]) and np.array_equal(bd, g["reflection_D"])
+
+
+def test_gpu_spawn_area_and_diffuse(hb):
+    from paper_1910_01304_b200 import scenes
+    from paper_1910_01304_b200.waves import spawn_secondary
+    sc = scenes.make_scene("c1", resolution=(64, 64))
+    b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2)
+    O, D = scenes.primary_rays(sc.camera, 2, seed=0)
+    n = O.shape[0]
+    base = hb.intersect_closest_batch(b, O, D, np.zeros(n), np.full(n, np.inf))
+    w = spawn_secondary(b, O, D, base, shadow=("area", (0.0, 4.0, 0.0), 0.5), bounce="diffuse",
+                        seed=3)
+    _, P, N = scenes.hit_frames(O, D, base["found"], base["t"], base["slot"],
+                                scenes.slot_normals(b.tv0, b.tv1, b.tv2))
+    lp = scenes.area_light_samples(P.shape[0], (0.0, 4.0, 0.0), 0.5, seed=3)
+    ref = scenes.shadow_rays(P, lp)
+    got = [x.cpu().numpy() for x in w["shadow"]]
+    for a_, r_ in zip(got, ref):
+        assert np.array_equal(a_, r_)
+    rb = scenes.cosine_bounce(P, N, seed=3)
+    gb = [x.cpu().numpy() for x in w["bounce"]]
+    assert np.array_equal(gb[0], rb[0])
+    np.testing.assert_allclose(gb[1], rb[1], atol=2e-7)  # sin/cos: libm vs CUDA, last bits
