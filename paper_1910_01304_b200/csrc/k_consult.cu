@@ -97,6 +97,7 @@ struct ConsultArgs {
   uint8_t* need;  // live: rays (by index) whose full traversal is needed next
   int32_t* seg_f1;  // first sorted position of the segment that appends (or INT_MAX)
   int spec;       // live replay: 0 mark the first unknown ray, 2 mark every unresolved ray
+  int sparse_state;  // 1: eval0 stores no state for rays whose key had no entry
   const int* err;
 };
 
@@ -127,6 +128,19 @@ __device__ __forceinline__ void store_state(const ConsultArgs& a, int32_t pos, c
   s.applied = applied;
   s.found = acc.found;
   a.state[pos] = s;
+}
+
+// The state of a ray whose key had no entry at the wave start is the empty
+// entry result; with sparse_state it is never materialised.
+template <bool CLOSEST>
+__device__ __forceinline__ void get_state(const ConsultArgs& a, int32_t idx, int32_t ex_len,
+                                          Hit& acc, int32_t& applied) {
+  if (a.sparse_state && ex_len == 0) {
+    acc = empty_entry_result(CLOSEST);
+    applied = 0;
+  } else {
+    load_state(a, idx, acc, applied);
+  }
 }
 
 struct Tally {
@@ -237,10 +251,9 @@ __global__ void k_first_append(ConsultArgs a, int64_t n) {
   if (*a.err) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const RayState st = a.state[i];
     const int32_t s = a.seg_of_ray[i];
-    const int32_t ex_len = st.applied;  // eval0 folded exactly the wave-start entry
-    if (ex_len > 0 && st.found) continue;  // TP against the wave-start entry
+    const int32_t ex_len = a.seg_exlen[s];
+    if (ex_len > 0 && a.state[i].found) continue;  // TP against the wave-start entry
     if (!a.f_found[i]) continue;
     if (!in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[i]]))
       atomicMin(a.seg_f1 + s, (int32_t)i);
@@ -256,9 +269,10 @@ __global__ void __launch_bounds__(128) k_finalize(ConsultArgs a, int64_t n) {
     const int32_t s = a.seg_of_ray[i];
     const int32_t f1 = a.seg_f1[s];
     if (i > f1) continue;  // after the first append: replayed
+    const int32_t ex_len = a.seg_exlen[s];
     Hit acc;
-    int32_t ex_len;
-    load_state(a, (int32_t)i, acc, ex_len);
+    int32_t applied;
+    get_state<CLOSEST>(a, (int32_t)i, ex_len, acc, applied);
     if (ex_len > 0 && acc.found) commit_tp<CLOSEST, LIVE>(a, c, (int32_t)i, acc);
     else commit_miss<LIVE>(a, c, (int32_t)i, acc, ex_len == 0);
     if (i == f1) {  // the first record(key, anc[leaf]) of this segment
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__(128) k_eval0(ConsultArgs a, int64_t n, int mar
       const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
       catch_up<CLOSEST, STACK>(a, r, acc, 0, ex_len, a.seg_exoff[s], ex_len, nullptr);
     }
-    store_state(a, (int32_t)i, acc, ex_len);
+    if (ex_len > 0 || !a.sparse_state) store_state(a, (int32_t)i, acc, ex_len);
     if (mark_need) a.need[i] = !(ex_len > 0 && acc.found);
   }
 }
@@ -359,7 +373,7 @@ __device__ void seg_thread(const ConsultArgs& a, Tally& c, int s, int32_t beg, i
     const int32_t idx = a.sidx[j];
     Hit acc;
     int32_t applied;
-    load_state(a, idx, acc, applied);
+    get_state<CLOSEST>(a, idx, ex_len, acc, applied);
     const int32_t L = ex_len + napp;
     if (applied < L && (CLOSEST || !acc.found)) {
       const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
@@ -408,7 +422,7 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
     const int32_t idx = valid ? a.sidx[pos] : 0;
     Hit acc = empty_entry_result(CLOSEST);
     int32_t applied = 0;
-    if (valid) load_state(a, idx, acc, applied);
+    if (valid) get_state<CLOSEST>(a, idx, ex_len, acc, applied);
     int32_t L = ex_len + napp;
     const bool fknown = valid && (!LIVE || a.f_known[idx]);
     int32_t cnode = -1;
@@ -552,7 +566,7 @@ __global__ void __launch_bounds__(128) k_replay_group(ConsultArgs a, const int32
   const int32_t idx = valid ? a.sidx[pos] : 0;
   Hit acc = empty_entry_result(CLOSEST);
   int32_t applied = 0;
-  if (valid) load_state(a, idx, acc, applied);
+  if (valid) get_state<CLOSEST>(a, idx, ex_len, acc, applied);
   int32_t L = ex_len + napp;
   int32_t cnode = -1;
   if (valid && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
@@ -867,6 +881,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     HRPP_LAUNCHED();
   }
   const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;
+  // suspend/resume rounds store states for every ray; the default path does not
+  a.sparse_state = !(c.live && rounds > 0);
   if (c.live) {
     uint8_t *f_found, *f_known;
     double* f_t;
