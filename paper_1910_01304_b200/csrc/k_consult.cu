@@ -155,7 +155,7 @@ __device__ __forceinline__ int32_t entry_node(const ConsultArgs& a, int64_t ex_o
 
 // Fold entry nodes [from, L) into acc: eval_entry_{closest,any}, resumable.
 template <bool CLOSEST, int STACK>
-__device__ __noinline__ void catch_up(const ConsultArgs& a, const Ray& r, Hit& acc, int32_t from,
+__device__ __forceinline__ void catch_up(const ConsultArgs& a, const Ray& r, Hit& acc, int32_t from,
                                       int32_t L, int64_t ex_off, int32_t ex_len,
                                       const int32_t* app) {
   for (int32_t j = from; j < L; j++) {
