@@ -255,6 +255,10 @@ int hrpp_set_trace_persistent(int on) {
   g_trace_persistent = on != 0;
   return HRPP_OK;
 }
+int hrpp_set_trace_coherent(int on) {
+  g_trace_coherent = on != 0;
+  return HRPP_OK;
+}
 int hrpp_set_consult_short(int len) {
   CHECK_ARG(len >= 0, "short segment length must be >= 0");
   g_consult_short = len;
@@ -401,6 +405,10 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
   h->height = height;
   h->stack = stack;
   h->parent_host.assign(parent, parent + n_nodes);
+  for (int k = 0; k < 3; k++) {
+    h->root_lo[k] = bmin[k];
+    h->root_hi[k] = bmax[k];
+  }
   bool ok = cudaMalloc(&h->nodes, sizeof(DNode) * n_nodes) == cudaSuccess &&
             cudaMalloc(&h->tris, sizeof(DTri) * ht.size()) == cudaSuccess &&
             cudaMalloc(&h->depth, sizeof(int32_t) * n_nodes) == cudaSuccess &&
@@ -464,7 +472,7 @@ int hrpp_trace_batch(hrpp_bvh_t bvh, int kind, const float* O, const float* D,
     if ((rc = sg.out(out->u, n, &to.u)) || (rc = sg.out(out->v, n, &to.v))) return rc;
   }
   if ((rc = launch_trace(*bvh, closest, dO, dD, d0, d1, start, n, nullptr, nullptr, to, nullptr,
-                         st)))
+                         st, &global_ws())))
     return rc;
   return sg.finish();
 }
@@ -707,7 +715,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
   if (mode != HRPP_MODE_LIVE) {
     to.sums = sdev + 4;  // baseline_box_tests, baseline_tri_tests (tracer.py:361-362)
     if ((rc = launch_trace(*bvh, closest != 0, dO, dD, d0, d1, 0, n, nullptr, nullptr, to, err,
-                           st)))
+                           st, &ws)))
       return rc;
   }
   if (mode != HRPP_MODE_BASELINE) {

@@ -78,6 +78,7 @@ struct BvhDev {
   int32_t* tri_ids = nullptr;
   int64_t n_nodes = 0, n_tris = 0;
   int height = 0;      // longest root-to-leaf edge count (stack bound)
+  float root_lo[3] = {0, 0, 0}, root_hi[3] = {1, 1, 1};  // scene bounds (coherence keys)
   int stack = 64;      // template stack size chosen from height
   std::vector<int32_t> parent_host;
   std::map<int, int32_t*> anc;  // go-up level -> device LUT
@@ -119,10 +120,15 @@ int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys
                 cudaStream_t st);
 int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err,
                        cudaStream_t st);
+// Traces n rays (or the device-counted queue ray_idx[0..*count_dev)).  With
+// g_trace_coherent, large batches are traced in a coherence order (direction
+// octant, quantized direction, origin Morton code) -- a permutation of the
+// work only; every ray's result is unchanged.
 int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const double* tmin, const double* tmax, int32_t start, int64_t n,
                  const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
-                 const int* err, cudaStream_t st);
+                 const int* err, cudaStream_t st, Workspace* ws = nullptr);
+extern int g_trace_coherent;
 
 // Group a batch of keys: stable sort (key, ray) and find key segments.
 struct Segments {

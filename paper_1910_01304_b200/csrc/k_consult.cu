@@ -936,7 +936,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       // is worse: the xor-mixed key scatters unrelated rays into one warp)
       if ((rc = compact_flags(ws, a.need, n, queue, qcount, st))) return rc;
       if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, queue, qcount, to,
-                             err, st)))
+                             err, st, &ws)))
         return rc;
     }
     a.spec = 0;

@@ -1,4 +1,8 @@
 // k_hash_trace.cu -- ray hash kernel and full-traversal batch kernel.
+#include <cstdlib>
+
+#include <cub/cub.cuh>
+
 #include "hrpp_internal.h"
 
 namespace hrpp {
@@ -332,11 +336,101 @@ static void dispatch_trace(int stack, int grid, cudaStream_t st, const TraceArgs
   }
 }
 
+// ---------------------------------------------------------------------------
+// Coherence order for traversal: 32-bit key = direction octant (3 bits) |
+// Morton-interleaved direction (3 bits/axis) | Morton-interleaved origin in
+// the scene box (6 bits/axis, 18 bits).  Sorting only permutes which lanes
+// trace which rays.
+// ---------------------------------------------------------------------------
+
+int g_trace_coherent = 0;
+static int coh_begin_bit() {  // radix passes = ceil((30 - begin) / 8)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HRPP_COH_BEGIN_BIT");
+    v = e ? atoi(e) : 14;
+    if (v < 0 || v > 29) v = 14;
+  }
+  return v;
+}
+constexpr int64_t kCoherentMin = 1 << 16;  // smaller batches trace in the given order
+
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {  // 10 bits -> every third bit
+  x &= 0x3FF;
+  x = (x | (x << 16)) & 0x30000FF;
+  x = (x | (x << 8)) & 0x300F00F;
+  x = (x | (x << 4)) & 0x30C30C3;
+  x = (x | (x << 2)) & 0x9249249;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t quant(float v, float lo, float inv, uint32_t maxq) {
+  float q = (v - lo) * inv;
+  q = q < 0.f ? 0.f : q;
+  uint32_t u = (uint32_t)q;
+  return u > maxq ? maxq : u;
+}
+
+__global__ void k_coh_key(const float* __restrict__ O, const float* __restrict__ D,
+                          const int32_t* __restrict__ ray_idx, const int* count_dev, int64_t n,
+                          float3 lo, float3 inv, uint32_t* keys, int32_t* vals) {
+  const int64_t count = count_dev ? (int64_t)*count_dev : n;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    if (q >= count) {  // padding sorts last and is never traced
+      keys[q] = 0xFFFFFFFFu;
+      vals[q] = 0;
+      continue;
+    }
+    const int64_t i = ray_idx ? (int64_t)ray_idx[q] : q;
+    const float dx = D[3 * i], dy = D[3 * i + 1], dz = D[3 * i + 2];
+    const uint32_t oct = (dx < 0.f) | ((dz < 0.f) << 1) | ((dy < 0.f) << 2);
+    const uint32_t dq = spread3(quant(dx, -1.f, 4.f, 7)) | (spread3(quant(dy, -1.f, 4.f, 7)) << 1) |
+                        (spread3(quant(dz, -1.f, 4.f, 7)) << 2);
+    const uint32_t oq = spread3(quant(O[3 * i], lo.x, inv.x, 63)) |
+                        (spread3(quant(O[3 * i + 1], lo.y, inv.y, 63)) << 1) |
+                        (spread3(quant(O[3 * i + 2], lo.z, inv.z, 63)) << 2);
+    keys[q] = (oct << 27) | (dq << 18) | oq;
+    vals[q] = (int32_t)i;
+  }
+}
+
 int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const double* tmin, const double* tmax, int32_t start, int64_t n,
                  const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
-                 const int* err, cudaStream_t st) {
+                 const int* err, cudaStream_t st, Workspace* ws) {
   if (n <= 0) return 0;
+  if (g_trace_coherent && ws && n >= kCoherentMin) {
+    uint32_t *keys, *keys2;
+    int32_t *vals, *order;
+    int rc;
+    if ((rc = ws->get("coh_k", n, &keys)) || (rc = ws->get("coh_k2", n, &keys2)) ||
+        (rc = ws->get("coh_v", n, &vals)) || (rc = ws->get("coh_o", n, &order)))
+      return rc;
+    float3 lo, inv;
+    lo.x = b.root_lo[0];
+    lo.y = b.root_lo[1];
+    lo.z = b.root_lo[2];
+    const float ex = b.root_hi[0] - b.root_lo[0], ey = b.root_hi[1] - b.root_lo[1],
+                ez = b.root_hi[2] - b.root_lo[2];
+    inv.x = ex > 0.f ? 64.f / ex : 0.f;
+    inv.y = ey > 0.f ? 64.f / ey : 0.f;
+    inv.z = ez > 0.f ? 64.f / ez : 0.f;
+    size_t bytes = 0;
+    const int bb = coh_begin_bit();
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, vals, order, (int)n, bb, 30, st);
+    void* tmp;
+    if ((rc = ws->get_raw("coh_tmp", bytes, &tmp))) return rc;
+    {
+      ProfScope ps(P_GROUP, st);
+      k_coh_key<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(O, D, ray_idx, count_dev, n, lo,
+                                                                  inv, keys, vals);
+      HRPP_LAUNCHED();
+      HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys2, vals, order, (int)n, bb, 30,
+                                              st));
+    }
+    ray_idx = order;
+  }
   TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
   ProfScope ps(ray_idx ? P_TRACE_QUEUE : P_TRACE, st);
   if (g_trace_persistent) {
