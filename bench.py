@@ -69,38 +69,49 @@ def parse():
 # ---------------------------------------------------------------------------
 
 def make_workload(args, trace_closest=None):
-    """Scene, BVH arrays and the three waves of one frame (host numpy).
+    """Scene, BVH and the ordered waves of one frame (host numpy).
 
-    Secondary waves are spawned from the full-traversal hits of the primary
-    wave; `trace_closest(O, D)` supplies them (GPU in our arm, the oracle in
-    the reference arm) -- the result is identical either way (bit-exact)."""
+    Waves: the primary wave; shadow rays (one wave per light) from its hits;
+    then for every diffuse bounce b = 1..B the bounce wave spawned from the
+    previous closest-hit wave, followed by its shadow waves except after the
+    last bounce.  `trace_closest` gives the full-traversal hits used for
+    spawning (GPU in our arm, the oracle in the reference arm; bit-identical).
+    Returns [(name, kind, closest, O, D, tmin, tmax), ...]."""
     import paper_1910_01304_b200 as hb
     from paper_1910_01304_b200 import scenes
     res = tuple(int(x) for x in args.res.split("x")) if args.res else None
     sc = scenes.make_scene(args.config, resolution=res, spp=args.spp)
     bvh = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
+    normals = scenes.slot_normals(bvh.tv0, bvh.tv1, bvh.tv2)
     O, D = scenes.primary_rays(sc.camera, sc.spp, seed=0)
     n = O.shape[0]
-    t0, t1 = np.zeros(n), np.full(n, np.inf)
-    base = trace_closest(bvh, O, D, t0, t1)
-    normals = scenes.slot_normals(bvh.tv0, bvh.tv1, bvh.tv2)
-    _, P, N = scenes.hit_frames(O, D, base["found"], base["t"], base["slot"], normals)
-    if sc.area_light is not None:
-        lp = scenes.area_light_samples(P.shape[0], sc.area_light[0], sc.area_light[1], seed=0)
-    else:
-        lp = np.broadcast_to(np.asarray(sc.point_lights[0], np.float64), P.shape)
-    waves = {"primary": (True, O, D, t0, t1),
-             "shadow": (False, *scenes.shadow_rays(P, lp)),
-             "bounce": (True, *scenes.cosine_bounce(P, N, seed=0))}
+    waves = [("primary", "primary", True, O, D, np.zeros(n), np.full(n, np.inf))]
+    cur = waves[0]
+    for level in range(sc.bounces + 1):
+        _, _, _, Oc, Dc, t0, t1 = cur
+        base = trace_closest(bvh, Oc, Dc, t0, t1)
+        _, P, N = scenes.hit_frames(Oc, Dc, base["found"], base["t"], base["slot"], normals)
+        if level < sc.bounces or level == 0:
+            if sc.area_light is not None:
+                lps = [scenes.area_light_samples(P.shape[0], sc.area_light[0], sc.area_light[1],
+                                                 seed=level)]
+            else:
+                lps = [np.broadcast_to(np.asarray(lp, np.float64), P.shape)
+                       for lp in sc.point_lights]
+            for li, lp in enumerate(lps):
+                waves.append((f"shadow{level}_{li}", "shadow", False, *scenes.shadow_rays(P, lp)))
+        if level < sc.bounces:
+            cur = (f"bounce{level + 1}", "bounce", True, *scenes.cosine_bounce(P, N, seed=level))
+            waves.append(cur)
     return sc, bvh, waves
 
 
 def shard(wave, rank, world):
     """Contiguous ray block of this rank (never interleave: SURVEY 8(e))."""
-    closest, O, D, t0, t1 = wave
+    name, kind, closest, O, D, t0, t1 = wave
     n = O.shape[0]
     lo, hi = (n * rank) // world, (n * (rank + 1)) // world
-    return closest, O[lo:hi], D[lo:hi], t0[lo:hi], t1[lo:hi]
+    return name, kind, closest, O[lo:hi], D[lo:hi], t0[lo:hi], t1[lo:hi]
 
 
 # ---------------------------------------------------------------------------
@@ -187,30 +198,25 @@ def run_ours(args, rank, world, local_rank):
     cfg = hb.HashConfig(args.precision)
     tables = {True: hb.PredictorTable(cfg, args.go_up, hb.RayKind.CLOSEST_HIT, device=local_rank),
               False: hb.PredictorTable(cfg, args.go_up, hb.RayKind.HIT_ANY, device=local_rank)}
-    my = {k: shard(w, rank, world) for k, w in waves.items()}
-    offsets = {k: (waves[k][1].shape[0] * rank) // world for k in KINDS}
-    dwaves = {}
-    for k, (closest, *arrs) in my.items():
-        dwaves[k] = (closest, *(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs))
-    n_local = sum(w[1].shape[0] for w in dwaves.values())
-    n_total = sum(w[1].shape[0] for w in waves.values())
+    my = [shard(w, rank, world) for w in waves]
+    offsets = [(w[3].shape[0] * rank) // world for w in waves]
+    to_dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    dwaves = [(w[2], *(to_dev(a) for a in w[3:])) for w in my]
+    n_local = sum(w[1].shape[0] for w in dwaves)
+    n_total = sum(w[3].shape[0] for w in waves)
+    kinds = sorted({w[1] for w in waves}, key=KINDS.index)
     stream = torch.cuda.current_stream()
 
     def frame(mode, stats=None, host=None):
         for t in tables.values():
             t.clear()
-        res = {}
-        for k in KINDS:
-            closest, O, D, t0, t1 = dwaves[k] if host is None else host[k]
-            st = stats[k] if stats is not None else None
-            out, st = hb.trace_wave(bvh, tables[closest] if mode != "baseline" else None, mode,
-                                    O, D, t0, t1, closest, stats=st,
-                                    outputs=None if host is None else host[k + "_out"],
-                                    defer_commit=world > 1 and mode != "baseline")
+        for j, (closest, O, D, t0, t1) in enumerate(dwaves if host is None else host["in"]):
+            st = stats[waves[j][1]] if stats is not None else None
+            hb.trace_wave(bvh, tables[closest] if mode != "baseline" else None, mode, O, D, t0, t1,
+                          closest, stats=st, outputs=None if host is None else host["out"][j],
+                          defer_commit=world > 1 and mode != "baseline")
             if world > 1 and mode != "baseline":
-                merge_wave_records(tables[closest], dist, ray_offset=offsets[k])
-            res[k] = (out, st)
-        return res
+                merge_wave_records(tables[closest], dist, ray_offset=offsets[j])
 
     def barrier():
         if world > 1:
@@ -255,48 +261,47 @@ def run_ours(args, rank, world, local_rank):
     value = n_total * args.steps / (ms_live * 1e-3) / 1e6
 
     # stats of one live frame (identical every frame: fresh tables, same rays)
-    live_stats = {k: np.zeros(11, np.int64) for k in KINDS}
+    live_stats = {k: np.zeros(11, np.int64) for k in kinds}
     frame("live", stats=live_stats)
+    stored_live = sum(int(t.stored_node_count) for t in tables.values())
 
     # ---- full traversal (baseline mode) and exact savings (limit mode) ---------------
     for _ in range(2):
         frame("baseline")
     ms_base = timed(lambda: frame("baseline"), args.steps)
     base_value = n_total * args.steps / (ms_base * 1e-3) / 1e6
-    lim_stats = {k: np.zeros(11, np.int64) for k in KINDS}
+    lim_stats = {k: np.zeros(11, np.int64) for k in kinds}
     frame("limit", stats=lim_stats)
+    tstats = {("closest" if c else "hit_any"): hb.table_stats(t) for c, t in tables.items()}
     if world > 1:
-        for k in KINDS:
-            t = torch.from_numpy(lim_stats[k]).to(dev)
-            dist.all_reduce(t)
-            lim_stats[k] = t.cpu().numpy()
-            t = torch.from_numpy(live_stats[k]).to(dev)
-            dist.all_reduce(t)
-            live_stats[k] = t.cpu().numpy()
+        for d_ in (lim_stats, live_stats):
+            for k in kinds:
+                t = torch.from_numpy(d_[k]).to(dev)
+                dist.all_reduce(t)
+                d_[k] = t.cpu().numpy()
 
     def pct(a, b):
         return 100.0 * a / b if b else 0.0
 
-    savings = {k: round(pct(lim_stats[k][8], lim_stats[k][4]), 4) for k in KINDS}
-    base_boxes = sum(int(lim_stats[k][4]) for k in KINDS)
-    live_boxes = sum(int(live_stats[k][4] + live_stats[k][6]) for k in KINDS)
+    savings = {k: round(pct(lim_stats[k][8], lim_stats[k][4]), 4) for k in kinds}
+    base_boxes = sum(int(lim_stats[k][4]) for k in kinds)
+    live_boxes = sum(int(live_stats[k][4] + live_stats[k][6]) for k in kinds)
     visit_reduction = 100.0 * (1.0 - live_boxes / base_boxes) if base_boxes else 0.0
 
     # ---- roofline of the dominant stage -------------------------------------------------
     steps = args.steps
     per_frame = {k: (v[0] / steps, v[1] / steps) for k, v in prof.items()}
-    rays_frame = n_local
-    s_live = {i: sum(int(live_stats[k][i]) for k in KINDS) // world for i in range(11)}
-    ntp = s_live[1]
+    s_live = {i: sum(int(live_stats[k][i]) for k in kinds) // world for i in range(11)}
     n_fallback = s_live[2] + s_live[3]
-    alg = {  # algorithmic bytes per frame (DESIGN.md "Roofline")
-        "hash": 32 * rays_frame,
+    alg = {  # algorithmic bytes per frame (DESIGN.md "Kernels")
+        "hash": 32 * n_local,
         "trace_queue": 64 * n_fallback + 32 * s_live[4] + 36 * s_live[5],
-        "consult": 72 * rays_frame + 36 * s_live[6] + 36 * s_live[7]
-                   + 32 * sum(int(tables[c].stored_node_count) for c in (True, False)),
+        "consult": 72 * n_local + 36 * s_live[6] + 36 * s_live[7] + 32 * stored_live,
     }
-    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    peak = (json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+            if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0)
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (measured copy)"
+                if (ROOT / "MEASURED_PEAKS.json").exists() else "fallback 6650 GB/s")
     stages = {}
     for k, (ms, cnt) in per_frame.items():
         if cnt == 0:
@@ -309,29 +314,28 @@ def run_ours(args, rank, world, local_rank):
     dom = max((k for k in stages if k in alg), key=lambda k: stages[k]["ms_per_frame"])
     d_ms = per_frame[dom][0] / max(1, per_frame[dom][1])  # average launch duration
     d_bytes = alg[dom] / max(1, per_frame[dom][1])
-    traffic_path = ROOT / "profiles" / "traffic.json"
     traffic = None
-    if traffic_path.exists():
-        traffic = json.loads(traffic_path.read_text()).get(dom)
-    roofline = {"kernel": dom, "bound": "hbm", "achieved": round(d_bytes / (d_ms * 1e-3) / 1e9, 2),
-                "peak": peak, "unit": "GB/s",
-                "frac": round(d_bytes / (d_ms * 1e-3) / 1e9 / peak, 4), "traffic": traffic,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(dom)
+    achieved = d_bytes / (d_ms * 1e-3) / 1e9
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src}
 
     # ---- e2e: host buffers through the public API ------------------------------------
     e2e = None
     if not args.no_e2e:
-        host = {}
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        host = {"in": [], "out": []}
         h2d = d2h = 0
-        for k in KINDS:
-            closest, O, D, t0, t1 = my[k]
-            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa
-            host[k] = (closest, pin(O), pin(D), pin(t0), pin(t1))
-            n = O.shape[0]
-            host[k + "_out"] = {"found": torch.empty(n, dtype=torch.bool).pin_memory(),
+        for w in my:
+            n = w[3].shape[0]
+            host["in"].append((w[2], *(pin(a) for a in w[3:])))
+            host["out"].append({"found": torch.empty(n, dtype=torch.bool).pin_memory(),
                                 "t": torch.empty(n, dtype=torch.float64).pin_memory(),
                                 "slot": torch.empty(n, dtype=torch.int32).pin_memory(),
-                                "leaf": torch.empty(n, dtype=torch.int32).pin_memory()}
+                                "leaf": torch.empty(n, dtype=torch.int32).pin_memory()})
             h2d += n * 40
             d2h += n * 17
         frame("live", host=host)
@@ -356,18 +360,19 @@ def run_ours(args, rank, world, local_rank):
         cpu = cpu_reference_frame(bvh, waves, args)
 
     if rank == 0:
+        res = sc.camera.resolution
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_live / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded displaced icosphere scene + generated ray waves)",
-            "config": {"workload": f"{args.config}: {sc.n_tris} tris, "
-                                   f"{sc.camera.resolution[0]}x{sc.camera.resolution[1]} "
-                                   f"spp{sc.spp} primary + area-light shadow + diffuse bounce",
+            "config": {"workload": f"{args.config}: {sc.n_tris} tris, {res[0]}x{res[1]} spp"
+                                   f"{sc.spp}, {len(waves)} waves ("
+                                   + ", ".join(w[0] for w in waves) + ")",
                        "mode": "live (predict, else full traversal, train in ray order)",
                        "rays_per_step": n_total,
-                       "rays_per_wave": {k: int(waves[k][1].shape[0]) for k in KINDS},
+                       "rays_per_wave": {w[0]: int(w[3].shape[0]) for w in waves},
                        "bvh_nodes": bvh.node_count, "bvh_max_depth": bvh.max_depth,
                        "precision": args.precision, "go_up": args.go_up,
                        "parallelism": f"contiguous ray blocks x{world}",
@@ -376,8 +381,13 @@ def run_ours(args, rank, world, local_rank):
             "speedup_vs_full_traversal": round(value / base_value, 4),
             "nodes_skipped_percent": savings,
             "live_node_visit_reduction_percent": round(visit_reduction, 3),
-            "limit_stats": {k: dict(zip(STATS_NAMES, map(int, lim_stats[k]))) for k in KINDS},
-            "live_stats": {k: dict(zip(STATS_NAMES, map(int, live_stats[k]))) for k in KINDS},
+            "table_stats": {k: {"entries": v.entries, "stored_nodes": v.stored_nodes,
+                                "avg_nodes_per_entry": round(v.avg_nodes_per_entry, 4),
+                                "max_nodes_per_entry": v.max_nodes_per_entry,
+                                "memory_bytes": v.memory.total_bytes}
+                            for k, v in tstats.items()},
+            "limit_stats": {k: dict(zip(STATS_NAMES, map(int, lim_stats[k]))) for k in kinds},
+            "live_stats": {k: dict(zip(STATS_NAMES, map(int, live_stats[k]))) for k in kinds},
             "stages": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
@@ -403,17 +413,14 @@ def cpu_reference_frame(bvh, waves, args, steps=1):
     from oracle import oracle
     ob = _oracle_bvh(bvh)
     frac = args.cpu_sample
-    sample = {k: tuple(a[:max(1, int(len(a) * frac))] if i else a
-                       for i, a in enumerate(w)) for k, w in waves.items()}
-    n = sum(s[1].shape[0] for s in sample.values())
+    sample = [(w[2], *(a[:max(1, int(len(a) * frac))] for a in w[3:])) for w in waves]
+    n = sum(s_[1].shape[0] for s_ in sample)
     best = None
     for _ in range(steps):
         tabs = {c: oracle.OracleTable(args.precision, args.go_up, c) for c in (True, False)}
         t0 = time.perf_counter()
-        for k in KINDS:
-            closest, O, D, a, b = sample[k]
-            rc, _, _ = oracle.trace_wave(ob, tabs[closest], "live", closest, O, D, a, b,
-                                         threads=1)
+        for closest, O, D, a, b in sample:
+            rc, _, _ = oracle.trace_wave(ob, tabs[closest], "live", closest, O, D, a, b, threads=1)
             assert rc == 0
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
@@ -428,18 +435,16 @@ def cpu_reference_frame(bvh, waves, args, steps=1):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from oracle import oracle
-    import paper_1910_01304_b200 as hb  # host-side builder + generators only
 
     def cpu_trace(bvh, O, D, t0, t1):
         return _oracle_bvh(bvh).trace_batch(True, O, D, t0, t1, threads=0)
 
     sc, bvh, waves = make_workload(args, cpu_trace)
-    # each step: live frame over the prefix sample (a bounded sample of the workload)
     for _ in range(min(args.warmup, 1)):
         cpu_reference_frame(bvh, waves, args)
     t0 = time.perf_counter()
     vals = []
+    r = None
     for _ in range(args.steps):
         r = cpu_reference_frame(bvh, waves, args)
         vals.append(r["value"])
@@ -451,7 +456,8 @@ def run_reference(args, rank, world):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same seeded scene and waves as our arm)", "impl": "reference",
             "config": {"workload": f"{args.config}: {sc.n_tris} tris, prefix sample "
-                                   f"{args.cpu_sample:g} of each wave", "mode": "live"},
+                                   f"{args.cpu_sample:g} of each of {len(waves)} waves",
+                       "mode": "live"},
             "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": 1, "kind": "port",
                              "sample": r["sample"]},
             "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,

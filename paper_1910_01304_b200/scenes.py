@@ -239,6 +239,30 @@ def make_scene(name: str, resolution=None, spp=None) -> SceneSpec:
         m0, m1, m2 = _mesh_tris(v, f)
         cam = Camera((0.0, 0.3, 3.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 60.0, (1024, 1024))
         sc = SceneSpec(name, m0, m1, m2, cam, point_lights=[(2.0, 4.0, 2.0)], spp=8, bounces=1)
+    elif name == "c5":
+        # 4096 seeded instances (64 x 64 grid, jittered, random rotation and
+        # scale) of a 13k-triangle displaced mesh, flattened, plus a ground plane
+        rng = np.random.default_rng(5)
+        base_v, base_f = displaced_icosphere(5, seed=5, amplitude=0.2, octaves=2)
+        base_f = trim_faces(base_f, 13_000, seed=5)
+        bv = base_v.astype(np.float64)
+        inst = []
+        for i in range(4096):
+            gx, gz = i % 64, i // 64
+            R = _rotation(rng)
+            sc_ = rng.uniform(0.3, 0.7)
+            pos = np.array([(gx - 31.5) * 1.6 + rng.uniform(-0.3, 0.3), rng.uniform(0.0, 0.6),
+                            (gz - 31.5) * 1.6 + rng.uniform(-0.3, 0.3)])
+            inst.append(((bv @ R.T) * sc_ + pos).astype(np.float32))
+        verts = np.stack(inst)  # (4096, V, 3)
+        m0 = verts[:, base_f[:, 0]].reshape(-1, 3)
+        m1 = verts[:, base_f[:, 1]].reshape(-1, 3)
+        m2 = verts[:, base_f[:, 2]].reshape(-1, 3)
+        g0, g1, g2 = ground_quad(-0.8, 60.0)
+        cam = Camera((0.0, 14.0, 40.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 60.0, (1024, 1024))
+        sc = SceneSpec(name, np.concatenate([m0, g0]), np.concatenate([m1, g1]),
+                       np.concatenate([m2, g2]), cam, area_light=((0.0, 30.0, 0.0), 5.0),
+                       spp=8, bounces=3)
     else:
         raise ValueError(f"unknown scene config {name!r}")
     if resolution is not None:
