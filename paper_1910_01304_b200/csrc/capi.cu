@@ -353,22 +353,16 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
   HRPP_CK(cudaSetDevice(device));
   std::vector<DNode> hn(n_nodes);
   for (int64_t i = 0; i < n_nodes; i++) {
-    DNode& d = hn[i];
-    for (int a = 0; a < 3; a++) {
-      d.bmin[a] = bmin[3 * i + a];
-      d.bmax[a] = bmax[3 * i + a];
-    }
     if (left[i] < 0) {
       CHECK_ARG(first[i] >= 0 && count[i] >= 0 && (int64_t)first[i] + count[i] <= n_tris,
                 "leaf triangle range out of bounds");
-      d.a = ~first[i];
-      d.b = count[i];
+      pack_node(hn[i], bmin + 3 * i, bmax + 3 * i, ~first[i], count[i]);
     } else {
       CHECK_ARG(left[i] < n_nodes && right[i] >= 0 && right[i] < n_nodes,
                 "child index out of range");
       int ax = axis[i] == 1 ? 1 : (axis[i] == 2 ? 2 : 0);
-      d.a = left[i];
-      d.b = (int32_t)((uint32_t)right[i] | ((uint32_t)ax << 30));
+      pack_node(hn[i], bmin + 3 * i, bmax + 3 * i, left[i],
+                (int32_t)((uint32_t)right[i] | ((uint32_t)ax << 30)));
     }
   }
   // tree height from the root (stack bound); guards against cycles
@@ -390,14 +384,7 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
   int stack = choose_stack(height);
   CHECK_ARG(stack > 0, "BVH deeper than the 512-entry traversal stack");
   std::vector<DTri> ht(n_tris > 0 ? n_tris : 1);
-  for (int64_t k = 0; k < n_tris; k++) {
-    const float* a = tv0 + 3 * k;
-    const float* b = tv1 + 3 * k;
-    const float* c = tv2 + 3 * k;
-    ht[k].p0 = make_float4(a[0], a[1], a[2], b[0]);
-    ht[k].p1 = make_float4(b[1], b[2], c[0], c[1]);
-    ht[k].p2 = make_float4(c[2], 0.f, 0.f, 0.f);
-  }
+  for (int64_t k = 0; k < n_tris; k++) pack_tri(ht[k], tv0 + 3 * k, tv1 + 3 * k, tv2 + 3 * k);
   auto* h = new hrpp_bvh_s();
   h->device = device;
   h->n_nodes = n_nodes;

@@ -17,16 +17,70 @@
 
 namespace hrpp {
 
-struct __align__(16) DNode {
+// HRPP_NODE_F64 (default 1): node boxes and triangle vertices are stored
+// pre-widened to float64 (exact), so the traversal loop does no f32->f64
+// conversions; 0 keeps the compact float32 records.
+#ifndef HRPP_NODE_F64
+#define HRPP_NODE_F64 1
+#endif
+
+#if HRPP_NODE_F64
+struct __align__(16) DNode {  // 64 B: four 16-B loads
+  double lo[3], hi[3];
+  int32_t a, b;
+  int64_t pad;
+};
+struct __align__(16) DTri {  // 80 B: five 16-B loads
+  double v[9];
+  double pad;
+};
+#else
+struct __align__(16) DNode {  // 32 B: two 16-B loads
   float bmin[3];
   int32_t a;
   float bmax[3];
   int32_t b;
 };
-
-struct __align__(16) DTri {
+struct __align__(16) DTri {  // 48 B: three 16-B loads
   float4 p0, p1, p2;
 };
+#endif
+
+// Host-side packing of the reference's arrays into the device records.
+__host__ __device__ inline void pack_node(DNode& d, const float* lo, const float* hi, int32_t a,
+                                          int32_t b) {
+#if HRPP_NODE_F64
+  for (int k = 0; k < 3; k++) {
+    d.lo[k] = lo[k];
+    d.hi[k] = hi[k];
+  }
+  d.a = a;
+  d.b = b;
+  d.pad = 0;
+#else
+  for (int k = 0; k < 3; k++) {
+    d.bmin[k] = lo[k];
+    d.bmax[k] = hi[k];
+  }
+  d.a = a;
+  d.b = b;
+#endif
+}
+
+__host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b, const float* c) {
+#if HRPP_NODE_F64
+  for (int k = 0; k < 3; k++) {
+    t.v[k] = a[k];
+    t.v[3 + k] = b[k];
+    t.v[6 + k] = c[k];
+  }
+  t.pad = 0.0;
+#else
+  t.p0 = make_float4(a[0], a[1], a[2], b[0]);
+  t.p1 = make_float4(b[1], b[2], c[0], c[1]);
+  t.p2 = make_float4(c[2], 0.f, 0.f, 0.f);
+#endif
+}
 
 constexpr double kDetEps = 1e-9;          // hrpp/kernels.py:20
 constexpr double kWrongClosestEps = 1e-9; // hrpp/tracer.py:52
@@ -44,45 +98,78 @@ __device__ __forceinline__ double recip(double d) {
   return d != 0.0 ? 1.0 / d : copysign(__longlong_as_double(0x7ff0000000000000LL), d);
 }
 
-__device__ __forceinline__ void load_node(const DNode* __restrict__ nodes, int32_t nd,
-                                          float4& lo, float4& hi) {
+struct NodeBox {
+  double lx, ly, lz, hx, hy, hz;
+  int32_t a, b;
+};
+
+__device__ __forceinline__ NodeBox load_node(const DNode* __restrict__ nodes, int32_t nd) {
+  NodeBox n;
+#if HRPP_NODE_F64
+  const double2* p = reinterpret_cast<const double2*>(nodes + nd);
+  const double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
+  const int4 q3 = __ldg(reinterpret_cast<const int4*>(nodes + nd) + 3);
+  n.lx = q0.x; n.ly = q0.y; n.lz = q1.x; n.hx = q1.y; n.hy = q2.x; n.hz = q2.y;
+  n.a = q3.x;
+  n.b = q3.y;
+#else
   const float4* p = reinterpret_cast<const float4*>(nodes + nd);
-  lo = __ldg(p);
-  hi = __ldg(p + 1);
+  const float4 lo = __ldg(p), hi = __ldg(p + 1);
+  n.lx = lo.x; n.ly = lo.y; n.lz = lo.z; n.hx = hi.x; n.hy = hi.y; n.hz = hi.z;
+  n.a = __float_as_int(lo.w);
+  n.b = __float_as_int(hi.w);
+#endif
+  return n;
 }
 
 // hrpp/kernels.py:23-51 (inclusive slab test; NaN compares are ignored)
-__device__ __forceinline__ bool box_hit(const float4& lo, const float4& hi, double ox, double oy,
-                                        double oz, double ivx, double ivy, double ivz, double t0,
+__device__ __forceinline__ bool box_hit(const NodeBox& n, double ox, double oy, double oz,
+                                        double ivx, double ivy, double ivz, double t0,
                                         double t1) {
   double tn = t0, tf = t1, a, b, s;
-  a = ((double)lo.x - ox) * ivx;
-  b = ((double)hi.x - ox) * ivx;
+  a = (n.lx - ox) * ivx;
+  b = (n.hx - ox) * ivx;
   if (ivx < 0.0) { s = a; a = b; b = s; }
   if (a > tn) tn = a;
   if (b < tf) tf = b;
-  a = ((double)lo.y - oy) * ivy;
-  b = ((double)hi.y - oy) * ivy;
+  a = (n.ly - oy) * ivy;
+  b = (n.hy - oy) * ivy;
   if (ivy < 0.0) { s = a; a = b; b = s; }
   if (a > tn) tn = a;
   if (b < tf) tf = b;
-  a = ((double)lo.z - oz) * ivz;
-  b = ((double)hi.z - oz) * ivz;
+  a = (n.lz - oz) * ivz;
+  b = (n.hz - oz) * ivz;
   if (ivz < 0.0) { s = a; a = b; b = s; }
   if (a > tn) tn = a;
   if (b < tf) tf = b;
   return tn <= tf;
 }
 
+// Triangle vertices widened to float64 (exact).
+__device__ __forceinline__ void load_tri(const DTri* __restrict__ tris, int32_t k, double v[9]) {
+#if HRPP_NODE_F64
+  const double2* p = reinterpret_cast<const double2*>(tris + k);
+  const double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
+  const double q4 = __ldg(reinterpret_cast<const double*>(tris + k) + 8);
+  v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y; v[4] = q2.x; v[5] = q2.y;
+  v[6] = q3.x; v[7] = q3.y; v[8] = q4;
+#else
+  const float4* p = reinterpret_cast<const float4*>(tris + k);
+  const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
+  v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y;
+  v[6] = q1.z; v[7] = q1.w; v[8] = q2.x;
+#endif
+}
+
 // hrpp/kernels.py:54-86 (Moller-Trumbore, |det| <= 1e-9 rejected)
 __device__ __forceinline__ bool tri_test(const DTri* __restrict__ tris, int32_t k, double ox,
                                          double oy, double oz, double dx, double dy, double dz,
                                          double& t, double& u, double& v) {
-  const float4* p = reinterpret_cast<const float4*>(tris + k);
-  float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
-  double ax = q0.x, ay = q0.y, az = q0.z;
-  double e1x = (double)q0.w - ax, e1y = (double)q1.x - ay, e1z = (double)q1.y - az;
-  double e2x = (double)q1.z - ax, e2y = (double)q1.w - ay, e2z = (double)q2.x - az;
+  double q[9];
+  load_tri(tris, k, q);
+  double ax = q[0], ay = q[1], az = q[2];
+  double e1x = q[3] - ax, e1y = q[4] - ay, e1z = q[5] - az;
+  double e2x = q[6] - ax, e2y = q[7] - ay, e2z = q[8] - az;
   double px = dy * e2z - dz * e2y;
   double py = dz * e2x - dx * e2z;
   double pz = dx * e2y - dy * e2x;
@@ -144,11 +231,10 @@ __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
   h.tris = 0;
   for (;;) {
     h.boxes++;
-    float4 lo, hi;
-    load_node(nodes, nd, lo, hi);
-    if (box_hit(lo, hi, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax)) {
-      const int32_t a = __float_as_int(lo.w);
-      const int32_t b = __float_as_int(hi.w);
+    const NodeBox nb = load_node(nodes, nd);
+    if (box_hit(nb, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax)) {
+      const int32_t a = nb.a;
+      const int32_t b = nb.b;
       if (a >= 0) {
         const int axis = (uint32_t)b >> 30;
         const int32_t right = b & 0x3FFFFFFF;

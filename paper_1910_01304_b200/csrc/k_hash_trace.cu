@@ -251,13 +251,11 @@ __global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_c
       for (int it = 0; it < HRPP_PERSIST_STEPS && top > 0; it++) {
         const int32_t nd = stack[--top];
         h.boxes++;
-        float4 lo, hi;
-        load_node(a.nodes, nd, lo, hi);
-        if (!box_hit(lo, hi, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin,
-                     CLOSEST ? h.t : r.tmax))
+        const NodeBox bx = load_node(a.nodes, nd);
+        if (!box_hit(bx, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax))
           continue;
-        const int32_t na = __float_as_int(lo.w);
-        const int32_t nb = __float_as_int(hi.w);
+        const int32_t na = bx.a;
+        const int32_t nb = bx.b;
         if (na < 0) {
           const int32_t f = ~na, e = f + nb;
           for (int32_t k = f; k < e; k++) {

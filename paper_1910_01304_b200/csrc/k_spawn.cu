@@ -114,11 +114,11 @@ __global__ void k_spawn(SpawnArgs a) {
     double P[3];
     for (int k = 0; k < 3; k++) P[k] = o[k] + t * d[k];
     // geometric normal of the slot (Bvh.slot_normals, hrpp/bvh.py:130-138)
-    const float4* q = reinterpret_cast<const float4*>(a.tris + a.slot[i]);
-    const float4 q0 = q[0], q1 = q[1], q2 = q[2];
-    const double v0[3] = {q0.x, q0.y, q0.z};
-    const double v1[3] = {q0.w, q1.x, q1.y};
-    const double v2[3] = {q1.z, q1.w, q2.x};
+    double q[9];
+    load_tri(a.tris, a.slot[i], q);
+    const double v0[3] = {q[0], q[1], q[2]};
+    const double v1[3] = {q[3], q[4], q[5]};
+    const double v2[3] = {q[6], q[7], q[8]};
     double e1[3], e2[3], N[3];
     for (int k = 0; k < 3; k++) {
       e1[k] = v1[k] - v0[k];
