@@ -831,7 +831,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   const int32_t* anc;
   if ((rc = const_cast<BvhDev&>(b).ancestor_lut(t.go_up, &anc))) return rc;
   Segments seg;
-  if ((rc = group_by_key(t.ws, keys, n, &seg, st))) return rc;
+  if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st))) return rc;
   // new entries <= key segments: read the segment count once so the hash
   // index stays sized to the table (L2-resident for c1-c3 tables), not to the wave
   int nsegs_h = 0;

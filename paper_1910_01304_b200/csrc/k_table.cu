@@ -23,21 +23,42 @@ __global__ void k_iota(int32_t* v, int64_t n) {
     v[i] = (int32_t)i;
 }
 
-__global__ void k_head_flags(const unsigned long long* __restrict__ sk, int64_t n,
-                             int32_t* __restrict__ flags) {
+// Hash keys use b = 1 + 2p bits of each 16-bit lane; packing the three lanes
+// contiguously (3b bits, 39 at p = 6) lets the radix sort skip the empty bits.
+__global__ void k_pack_keys(const unsigned long long* __restrict__ keys, int64_t n, int b,
+                            unsigned long long* __restrict__ packed, int32_t* __restrict__ iota) {
+  const unsigned long long m = (1ull << b) - 1ull;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    flags[i] = (i == 0) || (sk[i] != sk[i - 1]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    packed[i] = (k & m) | (((k >> 16) & m) << b) | (((k >> 32) & m) << (2 * b));
+    iota[i] = (int32_t)i;
+  }
+}
+
+// Segment heads of the sorted keys `src`; with b > 0 they are packed and are
+// written unpacked (48-bit hash keys) to `out`.
+__global__ void k_head_flags(const unsigned long long* __restrict__ src, int64_t n, int b,
+                             int32_t* __restrict__ flags, unsigned long long* __restrict__ out) {
+  const unsigned long long m = b ? (1ull << b) - 1ull : 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = src[i];
+    flags[i] = (i == 0) || (k != src[i - 1]);
+    if (b) out[i] = (k & m) | (((k >> b) & m) << 16) | (((k >> (2 * b)) & m) << 32);
+  }
 }
 
 __global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n) {
   seg_start[*nsegs] = (int32_t)n;
 }
 
-int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
+int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, Segments* seg,
                  cudaStream_t st) {
   int32_t* iota;
   int32_t* flags;
+  unsigned long long* packed = nullptr;
+  unsigned long long* sorted_out;
   int rc;
   if ((rc = ws.get("g_skeys", n, &seg->skeys))) return rc;
   if ((rc = ws.get("g_iota", n, &iota))) return rc;
@@ -48,12 +69,22 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
   if ((rc = ws.get("g_segid", n, &seg->seg_id))) return rc;
   int grid = grid_for(n, 256, num_sms() * 8);
   ProfScope ps(P_GROUP, st);
-  k_iota<<<grid, 256, 0, st>>>(iota, n);
-  HRPP_LAUNCHED();
   const unsigned long long* kin = reinterpret_cast<const unsigned long long*>(keys);
+  int end_bit = 64;  // generic keys (record API)
+  sorted_out = seg->skeys;
+  if (lane_bits > 0) {
+    if ((rc = ws.get("g_packed", n, &packed)) || (rc = ws.get("g_psorted", n, &sorted_out)))
+      return rc;
+    k_pack_keys<<<grid, 256, 0, st>>>(kin, n, lane_bits, packed, iota);
+    kin = packed;
+    end_bit = 3 * lane_bits;
+  } else {
+    k_iota<<<grid, 256, 0, st>>>(iota, n);
+  }
+  HRPP_LAUNCHED();
   size_t b_sort = 0, b_sel = 0, b_scan = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b_sort, kin, seg->skeys, iota, seg->sidx, (int)n,
-                                  0, 48, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, b_sort, kin, sorted_out, iota, seg->sidx, (int)n,
+                                  0, end_bit, st);
   cub::CountingInputIterator<int32_t> cnt(0);
   cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
                              st);
@@ -62,9 +93,9 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, Segments* seg,
   b = b > b_scan ? b : b_scan;
   void* tmp;
   if ((rc = ws.get_raw("g_cubtmp", b, &tmp))) return rc;
-  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b_sort, kin, seg->skeys, iota, seg->sidx, (int)n,
-                                          0, 48, st));
-  k_head_flags<<<grid, 256, 0, st>>>(seg->skeys, n, flags);
+  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b_sort, kin, sorted_out, iota, seg->sidx, (int)n,
+                                          0, end_bit, st));
+  k_head_flags<<<grid, 256, 0, st>>>(sorted_out, n, lane_bits, flags, seg->skeys);
   HRPP_LAUNCHED();
   HRPP_CK(cub::DeviceSelect::Flagged(tmp, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
                                      st));
@@ -525,7 +556,7 @@ int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_
   int rc;
   if ((rc = t.reserve(n, n, st))) return rc;
   Segments seg;
-  if ((rc = group_by_key(t.ws, keys, n, &seg, st))) return rc;
+  if ((rc = group_by_key(t.ws, keys, n, 0, &seg, st))) return rc;
   int32_t *app, *seg_eid, *seg_napp;
   if ((rc = t.ws.get("r_app", n, &app))) return rc;
   if ((rc = t.ws.get("r_eid", n, &seg_eid))) return rc;
