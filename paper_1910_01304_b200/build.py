@@ -1,6 +1,7 @@
 """Build the sm_100a shared library in-tree (paper_1910_01304_b200/lib/).
 
     python -m paper_1910_01304_b200.build [--force]
+    python -m paper_1910_01304_b200.build --variant NAME -DMACRO=V ...   (exp/NAME/)
 
 Each translation unit is compiled in parallel with nvcc for
 ``-gencode arch=compute_100a,code=sm_100a`` with ``--fmad=false`` (the
@@ -44,14 +45,14 @@ def _deps(src: Path):
             ROOT / "include" / "hrpp_b200.h"]
 
 
-def _compile(src: Path, verbose: bool):
-    obj = OBJ / (src.name + ".o")
+def _compile(src: Path, verbose: bool, objdir: Path = OBJ, defines=()):
+    obj = objdir / (src.name + ".o")
     if obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in _deps(src)
                             if d.exists()):
         return obj, ""
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *defines, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cpp":
-        cmd = [nvcc(), *NVCC_FLAGS, "-x", "c++", "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *defines, "-x", "c++", "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v") if src.suffix == ".cu" else None
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,27 +61,38 @@ def _compile(src: Path, verbose: bool):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OBJ.mkdir(parents=True, exist_ok=True)
-    LIB.parent.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str | None = None
+          ) -> Path:
+    """Build lib/libhrpp_b200.so; with ``variant`` build an experiment copy
+    with extra ``-D`` flags into exp/<variant>/ (never the shipped library)."""
+    objdir, lib = OBJ, LIB
+    if variant:
+        objdir = ROOT / "exp" / variant / "obj"
+        lib = ROOT / "exp" / variant / "libhrpp_b200.so"
+        force = True
+    objdir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     if force:
-        for o in OBJ.glob("*.o"):
+        for o in objdir.glob("*.o"):
             o.unlink()
     srcs = [CSRC / s for s in SOURCES]
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        results = list(ex.map(lambda s: _compile(s, verbose, objdir, defines), srcs))
     objs = [r[0] for r in results]
     logs = "".join(r[1] for r in results)
     if logs and verbose:
         sys.stderr.write(logs)
-    if LIB.exists() and not force and all(LIB.stat().st_mtime >= o.stat().st_mtime for o in objs):
-        return LIB
-    cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static"]
+    if lib.exists() and not force and all(lib.stat().st_mtime >= o.stat().st_mtime for o in objs):
+        return lib
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else None
+    print(build(force="--force" in argv, verbose="-v" in argv,
+                defines=[a for a in argv if a.startswith("-D")], variant=var))

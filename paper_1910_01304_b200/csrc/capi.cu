@@ -2,6 +2,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -95,7 +96,10 @@ int BvhDev::ancestor_lut(int level, const int32_t** out) {
 }
 
 // ---- per-stage CUDA-event profiler --------------------------------------------
+// Calls may run concurrently from several host threads (one stream each, e.g.
+// waves on different tables); the profiler's shared state is under a mutex.
 bool g_prof_on = false;
+static std::mutex g_prof_mu;
 struct ProfState {
   std::vector<cudaEvent_t> pool;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
@@ -116,18 +120,23 @@ static ProfState g_prof;
 
 ProfScope::ProfScope(int c, cudaStream_t s) : cat(c), st(s) {
   if (!g_prof_on) return;
-  a = g_prof.get();
-  b = g_prof.get();
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    a = g_prof.get();
+    b = g_prof.get();
+  }
   cudaEventRecord(a, st);
 }
 
 ProfScope::~ProfScope() {
   if (!a) return;
   cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof.pending.emplace_back(cat, a, b);
 }
 
 void prof_flush() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   for (auto& p : g_prof.pending) {
     float ms = 0.f;
     cudaEventSynchronize(std::get<2>(p));
@@ -141,8 +150,10 @@ void prof_flush() {
   g_prof.pending.clear();
 }
 
+// Scratch for calls without a table (and host staging): one per host thread
+// and device, so concurrent calls from different threads never share it.
 static Workspace& global_ws() {
-  static Workspace ws[64];
+  static thread_local Workspace ws[64];
   int dev = 0;
   cudaGetDevice(&dev);
   return ws[dev & 63];
@@ -224,7 +235,7 @@ struct Pinned {
     return 0;
   }
 };
-static Pinned g_pinned;
+static thread_local Pinned g_pinned;  // per host thread (see global_ws)
 
 }  // namespace hrpp
 
@@ -271,6 +282,7 @@ int hrpp_profile_enable(int on) {
 int hrpp_profile_read(double* ms, int64_t* counts, int n, int reset) {
   cudaDeviceSynchronize();
   prof_flush();
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   for (int k = 0; k < n && k < P_NCAT; k++) {
     if (ms) ms[k] = g_prof.ms[k];
     if (counts) counts[k] = g_prof.count[k];

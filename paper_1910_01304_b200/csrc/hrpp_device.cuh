@@ -1,11 +1,12 @@
 // hrpp_device.cuh -- device data layout and the bit-exact f64 traversal core.
 //
 // Layout in HBM:
-//   DNode  32 B  {bmin.xyz, a | bmax.xyz, b}: two 16-B loads per visit.
+//   DNode  64 B  {double lo.xyz, hi.xyz; a, b}: four 16-B loads per visit.
 //          interior: a = left (>= 0), b = right | axis << 30
 //          leaf:     a = ~first (< 0, so the reference's `left < 0` test
 //                    becomes `a < 0`), b = count
-//   DTri   48 B  {v0.xyz v1.x | v1.yz v2.xy | v2.z pad}: three 16-B loads.
+//   DTri   80 B  {double v0.xyz v1.xyz v2.xyz}: five loads.
+//   (HRPP_NODE_F64=0: 32-B / 48-B float32 records, widened on load.)
 //
 // Arithmetic restates hrpp/kernels.py:23-206 operation by operation in
 // float64.  The whole library is compiled with --fmad=false so no
@@ -206,18 +207,25 @@ __device__ __forceinline__ Ray make_ray(const float* __restrict__ O, const float
   return r;
 }
 
+// Per-thread traversal stack in local memory.  (A shared-memory column per
+// thread measured 8-15 % slower: it takes L1 capacity from the node reads.)
+template <int STACK>
+struct LocalStack {
+  int32_t s[STACK];
+  __device__ __forceinline__ int32_t& operator[](int i) { return s[i]; }
+};
+
 // trace_closest / trace_any from `start` (hrpp/kernels.py:89-206).
 // Traversal order: pop, count visit + box test, leaf = slots [first,
 // first+count) in order, interior pushes far then near (near = left iff
 // d[axis] >= 0, so -0.0 goes left).
-template <bool CLOSEST, int STACK>
-__device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
-                                          const DTri* __restrict__ tris, const Ray& r,
-                                          int32_t start) {
+template <bool CLOSEST, typename Stack>
+__device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
+                                         const DTri* __restrict__ tris, const Ray& r,
+                                         int32_t start, Stack& stack) {
   // The reference pushes far then near and pops near next; visiting the near
   // child directly (only far goes to the stack) is the same visit order with
   // one local-memory store and load less per interior node.
-  int32_t stack[STACK];
   int top = 0;
   int32_t nd = start;
   Hit h;
@@ -263,6 +271,14 @@ __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
     nd = stack[--top];
   }
   return h;
+}
+
+template <bool CLOSEST, int STACK>
+__device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
+                                          const DTri* __restrict__ tris, const Ray& r,
+                                          int32_t start) {
+  LocalStack<STACK> st;
+  return trace_stk<CLOSEST>(nodes, tris, r, start, st);
 }
 
 // One step of eval_entry_{closest,any} (hrpp/kernels.py:251-297): fold the

@@ -217,6 +217,17 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
 // stage 1: per segment entry lookup, then per ray wave-start evaluation
 // ---------------------------------------------------------------------------
 
+// Minimum resident 128-thread blocks per SM (register caps) per kernel family.
+#ifndef HRPP_EVAL_MINB
+#define HRPP_EVAL_MINB 1
+#endif
+#ifndef HRPP_FIN_MINB
+#define HRPP_FIN_MINB 1
+#endif
+#ifndef HRPP_REPLAY_MINB
+#define HRPP_REPLAY_MINB 6  // 80 registers (measured: consult 4.66 -> 4.11 ms on c2)
+#endif
+
 __global__ void k_seg_lookup(ConsultArgs a, int64_t n) {
   const int ns = *a.nsegs;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
@@ -261,7 +272,7 @@ __global__ void k_first_append(ConsultArgs a, int64_t n) {
 }
 
 template <bool CLOSEST, bool LIVE>
-__global__ void __launch_bounds__(128) k_finalize(ConsultArgs a, int64_t n) {
+__global__ void __launch_bounds__(128, HRPP_FIN_MINB) k_finalize(ConsultArgs a, int64_t n) {
   if (*a.err) return;
   Tally c;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -320,7 +331,7 @@ __global__ void k_seg_scatter(ConsultArgs a, int64_t n) {
 // Every ray against the entry as it stood at the start of the wave; ray
 // order, so ray, state and flag accesses are coalesced.
 template <bool CLOSEST, int STACK>
-__global__ void __launch_bounds__(128) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
+__global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
   if (*a.err) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -495,7 +506,7 @@ __device__ void seg_warp(const ConsultArgs& a, Tally& c, int s, int lane) {
 
 // Short segments: thread t owns key segment t.
 template <bool CLOSEST, bool LIVE, int STACK>
-__global__ void __launch_bounds__(128) k_replay_short(ConsultArgs a, int short_len) {
+__global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_short(ConsultArgs a, int short_len) {
   if (*a.err) return;
   const int ns = *a.nsegs;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -517,7 +528,7 @@ __global__ void __launch_bounds__(128) k_replay_short(ConsultArgs a, int short_l
 
 // Long segments: one warp per segment of the compacted list.
 template <bool CLOSEST, bool LIVE, int STACK>
-__global__ void __launch_bounds__(128) k_replay_long(ConsultArgs a, const int32_t* list,
+__global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_long(ConsultArgs a, const int32_t* list,
                                                      const int* count) {
   if (*a.err) return;
   const int lane = threadIdx.x & 31;
@@ -539,7 +550,7 @@ __global__ void __launch_bounds__(128) k_replay_long(ConsultArgs a, const int32_
 // with at most G rays left (the rays after its first append), 32/G segments
 // per warp.  Within a group this is seg_warp's ballot loop.
 template <bool CLOSEST, bool LIVE, int STACK, int G>
-__global__ void __launch_bounds__(128) k_replay_group(ConsultArgs a, const int32_t* list,
+__global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultArgs a, const int32_t* list,
                                                       int count) {
   if (*a.err) return;
   const int lane = threadIdx.x & 31;

@@ -132,8 +132,16 @@ struct TraceArgs {
   TraceOut out;
 };
 
+// Register cap from the resident-block target: 7 x 128 threads -> 72
+// registers (measured best of 1, 5, 6, 7, 8 on c2: +6 % primary, +8 %
+// shadow, +13 % bounce over the uncapped 86).  A leaf-batched "while-while"
+// loop (warp-synchronous box and triangle phases) measured 40 % slower.
+#ifndef HRPP_TRACE_MINB
+#define HRPP_TRACE_MINB 7
+#endif
+
 template <bool CLOSEST, int STACK>
-__global__ void __launch_bounds__(128) k_trace(TraceArgs a) {
+__global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
   if (a.err && *a.err) return;
   // one ray per thread; with a device-side count (fallback queue) the grid is
   // sized for the host-known upper bound and surplus threads exit at once
@@ -196,13 +204,20 @@ __device__ __forceinline__ void store_hit(const TraceOut& o, int64_t i, const Hi
   if (o.known) o.known[i] = 1;
 }
 
+#ifndef HRPP_PERSIST_MINB
+#define HRPP_PERSIST_MINB 7
+#endif
+
 template <bool CLOSEST, int STACK>
-__global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_counter) {
+__global__ void __launch_bounds__(128, HRPP_PERSIST_MINB) k_trace_persist(TraceArgs a,
+                                                                          int* chunk_counter,
+                                                                          int refill_below) {
   if (a.err && *a.err) return;
   const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.n;
   const int lane = threadIdx.x & 31;
-  int32_t stack[STACK];
+  LocalStack<STACK> stack;
   int top = 0;
+  int32_t nd = -1;  // next node to box-test; -1 = lane idle
   Hit h;
   h.found = false; h.t = 0.0; h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0;
   h.boxes = 0; h.tris = 0;
@@ -213,7 +228,7 @@ __global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_c
   unsigned long long sb = 0, stt = 0;
   for (;;) {
     unsigned busy = __ballot_sync(0xffffffffu, cur >= 0);
-    if (more && __popc(busy) < kRefillBelow) {
+    if (more && __popc(busy) < refill_below) {
       unsigned idle = ~busy;
       while (idle && more) {
         if (c_lo >= c_hi) {
@@ -233,8 +248,8 @@ __global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_c
           const int64_t q = c_lo + rank;
           cur = a.ray_idx ? (int64_t)a.ray_idx[q] : q;
           r = make_ray(a.O, a.D, a.tmin, a.tmax, cur);
-          stack[0] = a.start;
-          top = 1;
+          nd = a.start;
+          top = 0;
           h.found = false;
           h.t = CLOSEST ? r.tmax : 0.0;
           h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0; h.boxes = 0; h.tris = 0;
@@ -247,40 +262,41 @@ __global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_c
     }
     if (!busy) break;
     if (cur >= 0) {
-      // up to kStepsPerRefill node visits of trace_from (hrpp/kernels.py:112-153)
-      for (int it = 0; it < HRPP_PERSIST_STEPS && top > 0; it++) {
-        const int32_t nd = stack[--top];
+      // up to HRPP_PERSIST_STEPS node visits of trace_stk (hrpp/kernels.py:112-153)
+      for (int it = 0; it < HRPP_PERSIST_STEPS && nd >= 0; it++) {
         h.boxes++;
         const NodeBox bx = load_node(a.nodes, nd);
-        if (!box_hit(bx, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax))
-          continue;
-        const int32_t na = bx.a;
-        const int32_t nb = bx.b;
-        if (na < 0) {
-          const int32_t f = ~na, e = f + nb;
+        if (box_hit(bx, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax)) {
+          if (bx.a >= 0) {
+            const int axis = (uint32_t)bx.b >> 30;
+            const int32_t right = bx.b & 0x3FFFFFFF;
+            const double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
+            stack[top++] = dval >= 0.0 ? right : bx.a;
+            nd = dval >= 0.0 ? bx.a : right;
+            continue;
+          }
+          const int32_t f = ~bx.a, e = f + bx.b;
+          bool stop = false;
           for (int32_t k = f; k < e; k++) {
             double t, u, v;
             h.tris++;
             if (tri_test(a.tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) &&
                 t >= r.tmin && t <= r.tmax) {
-              if (!CLOSEST || !h.found || t < h.t) {
-                h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
-              }
               if (!CLOSEST) {
-                top = 0;
+                h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+                stop = true;
                 break;
+              }
+              if (!h.found || t < h.t) {
+                h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
               }
             }
           }
-        } else {
-          const int axis = (uint32_t)nb >> 30;
-          const int32_t right = nb & 0x3FFFFFFF;
-          const double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
-          stack[top++] = dval >= 0.0 ? right : na;
-          stack[top++] = dval >= 0.0 ? na : right;
+          if (stop) top = 0;
         }
+        nd = top > 0 ? stack[--top] : -1;
       }
-      if (top == 0) {
+      if (nd < 0) {
         store_hit<CLOSEST>(a.out, cur, h);
         sb += h.boxes;
         stt += h.tris;
@@ -300,6 +316,11 @@ __global__ void __launch_bounds__(128) k_trace_persist(TraceArgs a, int* chunk_c
 
 template <bool CLOSEST, int STACK>
 static void launch_persist(cudaStream_t st, const TraceArgs& a, int* counter) {
+  static int refill = -1;
+  if (refill < 0) {
+    const char* e = getenv("HRPP_REFILL");
+    refill = e ? atoi(e) : kRefillBelow;
+  }
   static int per_sm = 0;  // resident blocks of this instantiation
   if (!per_sm &&
       (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_persist<CLOSEST, STACK>,
@@ -309,7 +330,7 @@ static void launch_persist(cudaStream_t st, const TraceArgs& a, int* counter) {
   const int64_t need = (a.n + 127) / 128;
   const int64_t res = (int64_t)num_sms() * per_sm;
   const int grid = (int)(res < need ? res : (need > 0 ? need : 1));
-  k_trace_persist<CLOSEST, STACK><<<grid, 128, 0, st>>>(a, counter);
+  k_trace_persist<CLOSEST, STACK><<<grid, 128, 0, st>>>(a, counter, refill);
 }
 
 template <bool CLOSEST>
