@@ -57,6 +57,10 @@ def parse():
                     help="fraction (prefix) of every wave timed on the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the distributed wave path (NCCL collectives) even at N = 1 (testing)")
+    ap.add_argument("--shard", default="keys", choices=["keys", "blocks"],
+                    help="N > 1: exact key sharding (all-to-all) or ray blocks + record merge")
     ap.add_argument("--live-rounds", type=int, default=None)
     ap.add_argument("--consult-short", type=int, default=None)
     ap.add_argument("--profile-only", action="store_true",
@@ -182,10 +186,12 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     import paper_1910_01304_b200 as hb
     from paper_1910_01304_b200 import _lib
-    from paper_1910_01304_b200.parallel import merge_wave_records
+    from paper_1910_01304_b200.parallel import (key_sharded_wave, merge_wave_records,
+                                                partition_by_owner)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    multi = world > 1 or args.force_dist  # distributed wave paths (collectives)
     if args.live_rounds is not None:
         hb.set_live_rounds(args.live_rounds)
     if args.consult_short is not None:
@@ -207,19 +213,32 @@ def run_ours(args, rank, world, local_rank):
     kinds = sorted({w[1] for w in waves}, key=KINDS.index)
     stream = torch.cuda.current_stream()
 
-    def frame(mode, stats=None, host=None):
+    keyed = multi and args.shard == "keys"
+
+    def run_wave(j, mode, O, D, t0, t1, stats=None, outputs=None):
+        """One wave of this rank: key-sharded (exact), or its ray block with
+        the deferred-record exchange, or (N = 1) the plain call."""
+        closest = waves[j][2]
+        table = tables[closest] if mode != "baseline" else None
+        if keyed and mode != "baseline":
+            def trace_fn(Oo, Do, a, b):
+                return hb.trace_wave(bvh, table, mode, Oo, Do, a, b, closest, stats=stats)
+            return key_sharded_wave(dist, trace_fn, lambda Oo, Do: hb.hash_rays(Oo, Do, cfg),
+                                    partition_by_owner, O, D, t0, t1, outputs=outputs)[0]
+        out, _ = hb.trace_wave(bvh, table, mode, O, D, t0, t1, closest, stats=stats,
+                               outputs=outputs, defer_commit=multi and mode != "baseline")
+        if multi and mode != "baseline":
+            merge_wave_records(table, dist, ray_offset=offsets[j])
+        return out
+
+    def frame(mode, stats=None):
         for t in tables.values():
             t.clear()
-        for j, (closest, O, D, t0, t1) in enumerate(dwaves if host is None else host["in"]):
-            st = stats[waves[j][1]] if stats is not None else None
-            hb.trace_wave(bvh, tables[closest] if mode != "baseline" else None, mode, O, D, t0, t1,
-                          closest, stats=st, outputs=None if host is None else host["out"][j],
-                          defer_commit=world > 1 and mode != "baseline")
-            if world > 1 and mode != "baseline":
-                merge_wave_records(tables[closest], dist, ray_offset=offsets[j])
+        for j, (closest, O, D, t0, t1) in enumerate(dwaves):
+            run_wave(j, mode, O, D, t0, t1, stats=stats[waves[j][1]] if stats is not None else None)
 
     def barrier():
-        if world > 1:
+        if multi:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -233,7 +252,7 @@ def run_ours(args, rank, world, local_rank):
         ev1.record(stream)
         barrier()
         ms = ev0.elapsed_time(ev1)
-        if world > 1:
+        if multi:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
@@ -272,8 +291,22 @@ def run_ours(args, rank, world, local_rank):
     base_value = n_total * args.steps / (ms_base * 1e-3) / 1e6
     lim_stats = {k: np.zeros(11, np.int64) for k in kinds}
     frame("limit", stats=lim_stats)
-    tstats = {("closest" if c else "hit_any"): hb.table_stats(t) for c, t in tables.items()}
-    if world > 1:
+    tstats = {}
+    for c, t in tables.items():
+        ts = hb.table_stats(t)
+        if keyed:  # disjoint key partitions: the union's stats
+            v = torch.tensor([ts.entries, ts.stored_nodes, ts.memory.entry_bytes,
+                              ts.memory.node_ref_bytes], dtype=torch.int64, device=dev)
+            mx = torch.tensor([ts.max_nodes_per_entry], dtype=torch.int64, device=dev)
+            dist.all_reduce(v)
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            e, sn, eb, nb = (int(x) for x in v.tolist())
+            ts = hb.TableStats(entries=e, stored_nodes=sn,
+                               avg_nodes_per_entry=sn / e if e else 0.0,
+                               max_nodes_per_entry=int(mx.item()),
+                               memory=hb.MemoryEstimate(entry_bytes=eb, node_ref_bytes=nb))
+        tstats["closest" if c else "hit_any"] = ts
+    if multi:
         for d_ in (lim_stats, live_stats):
             for k in kinds:
                 t = torch.from_numpy(d_[k]).to(dev)
@@ -368,11 +401,7 @@ def run_ours(args, rank, world, local_rank):
                 if i + 1 < len(items):
                     upload(i + 1)
                 stream.wait_event(ev_in[i])
-                closest = my[j][2]
-                hb.trace_wave(bvh, tables[closest], "live", *d_in[j], closest,
-                              outputs=d_out[j], defer_commit=world > 1)
-                if world > 1:
-                    merge_wave_records(tables[closest], dist, ray_offset=offsets[j])
+                run_wave(j, "live", *d_in[j], outputs=d_out[j])
                 done = torch.cuda.Event()
                 done.record(stream)
                 copy_back.wait_event(done)
@@ -389,7 +418,7 @@ def run_ours(args, rank, world, local_rank):
         run_e2e(e_steps)
         barrier()
         dt = time.perf_counter() - t0w
-        if world > 1:
+        if multi:
             t = torch.tensor([dt], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
@@ -420,7 +449,9 @@ def run_ours(args, rank, world, local_rank):
                        "rays_per_wave": {w[0]: int(w[3].shape[0]) for w in waves},
                        "bvh_nodes": bvh.node_count, "bvh_max_depth": bvh.max_depth,
                        "precision": args.precision, "go_up": args.go_up,
-                       "parallelism": f"contiguous ray blocks x{world}",
+                       "parallelism": (f"key sharding x{world} (exact; all-to-all of rays "
+                                       "to key owners)" if keyed else
+                                       f"contiguous ray blocks x{world}"),
                        "l2": "inputs > L2 (335 MB primary wave); no flush needed"},
             "full_traversal_mrays_s": round(base_value, 3),
             "speedup_vs_full_traversal": round(value / base_value, 4),
@@ -518,15 +549,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    multi = world > 1 or args.force_dist
+    if multi:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                rank=rank, world_size=world)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if multi:
             import torch.distributed as dist
             dist.destroy_process_group()
 

@@ -179,6 +179,16 @@ int hrpp_table_export(hrpp_table_t table, uint64_t *keys, int64_t *offsets, int3
 int hrpp_table_set_deferred(hrpp_table_t table, int on);
 int hrpp_table_pending(hrpp_table_t table, uint64_t *keys, int32_t *nodes, int32_t *rays,
                        int64_t cap, int64_t *count);
+/* Exact multi-GPU mode (key sharding): owner of key k among
+ * `world` ranks = (mix64(k) >> 32) % world.  perm (device int32[n]) receives
+ * the local rays grouped by owner, ray order kept within each owner (stable);
+ * counts (host int64[world]) the rays per owner.  After an all-to-all of the
+ * permuted rays every owner holds all rays of its keys in global ray order
+ * and its consult is the single-GPU consult restricted to those keys, so
+ * hits, statistics and the union of the tables equal one GPU's at any world
+ * size.  keys: device uint64[n] from hrpp_hash_rays. */
+int hrpp_partition_by_owner(const uint64_t *keys, int64_t n, int world, int32_t *perm,
+                            int64_t *counts, void *stream);
 
 /* ---- predict: hrpp/predictor.py:167-192 over a batch, frozen table ------ */
 /* cls 0 TP / 1 FP / 2 NEG; t/slot/leaf/u/v of the entry result (t = inf for
@@ -211,7 +221,7 @@ int hrpp_profile_enable(int on);
 int hrpp_profile_read(double *ms, int64_t *counts, int n, int reset);
 
 /* Live-mode speculation policy (rounds of exact per-key scan before the
- * speculative round).  Default 3.  Affects speed only, never results. */
+ * speculative round).  Default 0.  Affects speed only, never results. */
 int hrpp_set_live_rounds(int rounds);
 /* Key segments with at most `len` rays are replayed by one lane, longer ones
  * by a whole warp (default 32).  Affects speed only, never results. */

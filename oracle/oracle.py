@@ -126,6 +126,22 @@ def _lane_hash_np(bits, p):
     return (sign << np.uint32(2 * p)) | (exp_top << np.uint32(p)) | man_top
 
 
+def partition_by_owner_np(keys, world):
+    """CPU restatement of hrpp_partition_by_owner (k_shard.cu), the checker of
+    the key-sharded multi-GPU mode: owner = (mix64(key) >> 32) % world;
+    returns (stable permutation grouping rays by owner, counts per owner)."""
+    x = np.asarray(keys, np.uint64).copy()
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(33)
+        x *= np.uint64(0xff51afd7ed558ccd)
+        x ^= x >> np.uint64(33)
+        x *= np.uint64(0xc4ceb9fe1a85ec53)
+        x ^= x >> np.uint64(33)
+    owner = ((x >> np.uint64(32)) % np.uint64(world)).astype(np.int64)
+    perm = np.argsort(owner, kind="stable").astype(np.int32)
+    return perm, np.bincount(owner, minlength=world).astype(np.int64)
+
+
 def hash_rays_np(O, D, p):
     """numpy restatement of hrpp/rayhash.py:99-115; None on non-finite input."""
     bo = _c(O, np.float32).view(np.uint32).reshape(-1, 3)

@@ -247,7 +247,7 @@ extern "C" int hrpp_spawn(hrpp_bvh_t bvh, const float* O, const float* D, const 
   *count_out = 0;
   if (n == 0) return HRPP_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  static Workspace ws;
+  static thread_local Workspace ws;
   int32_t* pos;
   int* cnt;
   int rc;

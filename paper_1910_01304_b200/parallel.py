@@ -1,6 +1,16 @@
-"""Multi-GPU ray sharding with an exact-order predictor record exchange.
+"""Multi-GPU waves: exact key sharding, or ray blocks with a record exchange.
 
-Design: every rank holds the whole BVH
+Key sharding (``key_sharded_wave``, exact at any world size):
+the owner of key k is (mix64(k) >> 32) % world.  Each rank partitions its
+contiguous block of a wave by owner (stable, ``partition_by_owner`` on the
+device), one all-to-all moves every ray to the owner of its key, the owner
+runs the wave on its table partition, and a second all-to-all returns the
+hits.  Source blocks arrive in rank order, so each owner sees all rays of
+its keys in global ray order; a key's consult touches only its own entry
+(hrpp/tracer.py:233-267, 295-331), hence every hit, every statistic (summed
+over ranks) and the union of the table partitions equal one GPU's.
+
+Ray blocks (``merge_wave_records``, approximate): every rank holds the whole BVH
 and a local predictor table, and takes a CONTIGUOUS block of every wave
 (interleaving destroys within-wave training).  A rank consults its block in
 ray order against its table in deferred mode, so the table is not modified
@@ -17,6 +27,8 @@ costs < 0.5 pp of savings at 8 ranks (SURVEY 8(e) probe).
 from __future__ import annotations
 
 import numpy as np
+
+from . import _lib
 
 
 def block_range(n: int, rank: int, world: int):
@@ -77,3 +89,75 @@ def merge_wave_records(table, dist, ray_offset: int = 0, group=None):
     if mk.shape[0]:
         table.record_batch(mk, mn)
     return int(mk.shape[0])
+
+
+# ---------------------------------------------------------------------------
+# exact key sharding
+# ---------------------------------------------------------------------------
+
+def partition_by_owner(keys, world: int):
+    """(perm, counts): this rank's rays grouped by key owner, ray order kept
+    within each owner (hrpp_partition_by_owner).  ``keys`` is a CUDA uint64
+    tensor; perm is a CUDA int32 tensor, counts a host int64[world]."""
+    if not (_lib.is_torch(keys) and keys.is_cuda):
+        raise ValueError("partition_by_owner needs device keys (a CUDA tensor)")
+    n = int(keys.shape[0])
+    perm = _lib.empty(n, np.int32, like=keys)
+    counts = np.zeros(int(world), np.int64)
+    rc = _lib.lib.hrpp_partition_by_owner(_lib.ptr(keys), n, int(world), _lib.ptr(perm),
+                                          counts.ctypes.data_as(_lib.C.c_void_p),
+                                          _lib.stream_of(keys))
+    _lib.check(rc, "partition_by_owner")
+    return perm, counts
+
+
+def _a2a(dist, x, send_counts, recv_counts, group=None):
+    """all_to_all_single of the leading dimension with uneven splits."""
+    import torch
+    shape = (int(sum(recv_counts)),) + tuple(x.shape[1:])
+    flat = x.view(torch.uint8) if x.dtype == torch.bool else x
+    out = torch.empty(shape, dtype=flat.dtype, device=x.device)
+    dist.all_to_all_single(out, flat.contiguous(), [int(c) for c in recv_counts],
+                           [int(c) for c in send_counts], group=group)
+    return out.view(torch.bool) if x.dtype == torch.bool else out
+
+
+HIT_FIELDS = ("found", "t", "slot", "leaf")
+
+
+def key_sharded_wave(dist, trace_fn, key_fn, partition_fn, O, D, tmins, tmaxs, outputs=None,
+                     group=None):
+    """One wave over all ranks by key ownership (exact at any world size).
+
+    O, D (n,3) float32, tmins/tmaxs (n,) float64: this rank's CONTIGUOUS
+    block of the wave, blocks in rank order (``block_range``), as torch
+    tensors on the collective backend's device.  ``key_fn(O, D)`` hashes
+    (hrpp_hash_rays), ``partition_fn(keys, world)`` groups by owner
+    (``partition_by_owner``) and ``trace_fn(O, D, tmins, tmaxs)`` runs this
+    rank's table partition on the rays it owns (``trace_wave``) and returns
+    (hits dict, stats).  Returns (hits in this rank's ray order for
+    HIT_FIELDS, this rank's stats): the stats of all ranks sum to the
+    single-GPU stats.
+    """
+    import torch
+    world = dist.get_world_size(group)
+    keys = key_fn(O, D)
+    perm, counts = partition_fn(keys, world)
+    perm = torch.as_tensor(perm, device=O.device).long()
+    dev = O.device
+    send = torch.as_tensor(np.asarray(counts, np.int64), device=dev)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    send_counts = [int(c) for c in np.asarray(counts)]
+    recv_counts = [int(c) for c in recv.cpu().tolist()]
+    parts = [_a2a(dist, x.index_select(0, perm), send_counts, recv_counts, group)
+             for x in (O, D, tmins, tmaxs)]
+    hits, stats = trace_fn(*parts)
+    n = int(O.shape[0])
+    out = dict(outputs) if outputs else {}
+    for k in HIT_FIELDS:
+        back = _a2a(dist, torch.as_tensor(hits[k], device=dev), recv_counts, send_counts, group)
+        if k not in out:
+            out[k] = torch.empty(n, dtype=back.dtype, device=dev)
+        out[k].index_copy_(0, perm, back.to(out[k].dtype))
+    return out, stats

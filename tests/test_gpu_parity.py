@@ -539,3 +539,57 @@ def test_gpu_spawn_area_and_diffuse(hb):
     gb = [x.cpu().numpy() for x in w["bounce"]]
     assert np.array_equal(gb[0], rb[0])
     np.testing.assert_allclose(gb[1], rb[1], atol=2e-7)  # sin/cos: libm vs CUDA, last bits
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8, 256])
+def test_partition_by_owner_matches_restatement(hb, world, oracle_mod):
+    import torch
+    from paper_1910_01304_b200.parallel import partition_by_owner
+    rng = np.random.default_rng(world)
+    for n in (0, 1, 1000, 100003):
+        keys = rng.integers(0, 1 << 48, n, dtype=np.uint64)
+        perm, counts = partition_by_owner(torch.from_numpy(keys).cuda(), world)
+        rp, rc = oracle_mod.partition_by_owner_np(keys, world)
+        assert np.array_equal(perm.cpu().numpy(), rp) and np.array_equal(counts, rc)
+    with pytest.raises(ValueError):
+        partition_by_owner(torch.zeros(4, dtype=torch.uint64).cuda(), 0)
+
+
+@pytest.mark.parametrize("mode", ["limit", "live"])
+def test_key_sharding_invariant_one_gpu(hb, mode):
+    """The exact multi-GPU mode's premise on the device: running each owner's
+    rays (ray order kept) against its own table reproduces the full wave's
+    hits, summed stats and table, for a frame of three waves and 3 owners."""
+    import torch
+    from paper_1910_01304_b200.parallel import partition_by_owner
+    g = load_golden("wave_inputs.npz")
+    b = gbvh(hb, "spheres")
+    cfg = hb.HashConfig(6)
+    world = 3
+    full = {c: hb.PredictorTable(cfg, 0, hb.RayKind.CLOSEST_HIT if c else hb.RayKind.HIT_ANY)
+            for c in (True, False)}
+    own = [{c: hb.PredictorTable(cfg, 0, hb.RayKind.CLOSEST_HIT if c else hb.RayKind.HIT_ANY)
+            for c in (True, False)} for _ in range(world)]
+    for name, closest in (("primary", True), ("shadow", False), ("reflection", True)):
+        arrs = [torch.from_numpy(np.ascontiguousarray(g[f"{name}_{k}"])).cuda()
+                for k in ("O", "D", "tmin", "tmax")]
+        ref, rst = hb.trace_wave(b, full[closest], mode, *arrs, closest)
+        perm, counts = partition_by_owner(hb.hash_rays(arrs[0], arrs[1], cfg), world)
+        perm = perm.long()
+        tot = np.zeros(11, np.int64)
+        got = {k: torch.empty_like(ref[k]) for k in ("found", "t", "slot", "leaf")}
+        start = 0
+        for o in range(world):
+            idx = perm[start:start + int(counts[o])]
+            start += int(counts[o])
+            out, st = hb.trace_wave(b, own[o][closest], mode,
+                                    *(a.index_select(0, idx) for a in arrs), closest)
+            tot += st
+            for k in got:
+                got[k][idx] = out[k]
+        assert np.array_equal(tot, rst), name
+        for k in got:
+            assert torch.equal(got[k], ref[k]), (name, k)
+    for c in (True, False):
+        assert sorted(sum((list(t[c].dump_lines()) for t in own), [])) == \
+            list(full[c].dump_lines())
