@@ -147,6 +147,27 @@ struct Tally {
   long long tp = 0, fp = 0, neg = 0, ob = 0, ot = 0, sk = 0, est = 0, wr = 0, bb = 0, bt = 0;
 };
 
+// Add a block's tallies into the wave counters: warp sums, then one atomic
+// per counter per block (per-warp atomics on 10 shared addresses serialised
+// in L2).  Every thread of the block must call it.
+__device__ __forceinline__ void flush_tally(const Tally& c, unsigned long long* stats) {
+  __shared__ long long part[10][8];
+  const long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < 10; k++) {
+    const long long w = warp_sum(v[k]);
+    if (lane == 0) part[k][warp] = w;
+  }
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
+    long long sum = 0;
+    for (int w = 0; w < nw; w++) sum += part[threadIdx.x][w];
+    if (sum) atomicAdd(stats + slot[threadIdx.x], (unsigned long long)sum);
+  }
+}
+
 // The entry's j-th node: stored list first, then this wave's appends.
 __device__ __forceinline__ int32_t entry_node(const ConsultArgs& a, int64_t ex_off,
                                               int32_t ex_len, const int32_t* app, int32_t j) {
@@ -292,14 +313,7 @@ __global__ void __launch_bounds__(128, HRPP_FIN_MINB) k_finalize(ConsultArgs a, 
       a.app_ray[beg] = (int32_t)i;
     }
   }
-  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
-  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < 10; k++) {
-    long long w = warp_sum(v[k]);
-    if (lane == 0 && w) atomicAdd(a.stats + slot[k], (unsigned long long)w);
-  }
+  flush_tally(c, a.stats);
 }
 
 // Replay cursor per segment: right after its first append, or done.
@@ -516,14 +530,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_short(ConsultA
     const int32_t cur = a.seg_cursor[s];
     if (cur < end && end - beg <= short_len) seg_thread<CLOSEST, LIVE, STACK>(a, c, s, beg, end, cur);
   }
-  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
-  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < 10; k++) {
-    long long w = warp_sum(v[k]);
-    if (lane == 0 && w) atomicAdd(a.stats + slot[k], (unsigned long long)w);
-  }
+  flush_tally(c, a.stats);
 }
 
 // Long segments: one warp per segment of the compacted list.
@@ -537,13 +544,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_long(ConsultAr
   const int m = *count;
   Tally c;
   for (int k = w; k < m; k += nw) seg_warp<CLOSEST, LIVE, STACK>(a, c, list[k], lane);
-  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
-  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
-#pragma unroll
-  for (int k = 0; k < 10; k++) {
-    long long x = warp_sum(v[k]);
-    if (lane == 0 && x) atomicAdd(a.stats + slot[k], (unsigned long long)x);
-  }
+  flush_tally(c, a.stats);
 }
 
 // Grouped single-tile replay: a group of G lanes replays one key segment
@@ -622,13 +623,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
     a.seg_napp[s] = napp;
     a.seg_cursor[s] = end;
   }
-  long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
-  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
-#pragma unroll
-  for (int k = 0; k < 10; k++) {
-    long long w = warp_sum(v[k]);
-    if (lane == 0 && w) atomicAdd(a.stats + slot[k], (unsigned long long)w);
-  }
+  flush_tally(c, a.stats);
 }
 
 // Replay length class of every segment (rays left): 0 done, 1..6 for
@@ -821,12 +816,16 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
   ProfScope ps(P_CONSULT, st);
   k_first_append<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
   HRPP_LAUNCHED();
+  // about one resident wave of blocks: a thread walks several rays and each
+  // block flushes its tallies once
+  const int fgrid = grid_for(n, 128, num_sms() * 8);
+  (void)grid;
   if (closest) {
-    if (live) k_finalize<true, true><<<grid, 128, 0, st>>>(a, n);
-    else k_finalize<true, false><<<grid, 128, 0, st>>>(a, n);
+    if (live) k_finalize<true, true><<<fgrid, 128, 0, st>>>(a, n);
+    else k_finalize<true, false><<<fgrid, 128, 0, st>>>(a, n);
   } else {
-    if (live) k_finalize<false, true><<<grid, 128, 0, st>>>(a, n);
-    else k_finalize<false, false><<<grid, 128, 0, st>>>(a, n);
+    if (live) k_finalize<false, true><<<fgrid, 128, 0, st>>>(a, n);
+    else k_finalize<false, false><<<fgrid, 128, 0, st>>>(a, n);
   }
   HRPP_LAUNCHED();
   k_seg_cursor<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a);

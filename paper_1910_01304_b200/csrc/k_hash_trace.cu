@@ -166,12 +166,19 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     sb = h.boxes;
     stt = h.tris;
   }
-  if (a.out.sums) {
+  if (a.out.sums) {  // one atomic pair per block (a.out.sums is uniform)
+    __shared__ unsigned long long part[2][4];
     sb = warp_sum(sb);
     stt = warp_sum(stt);
-    if ((threadIdx.x & 31) == 0 && (sb | stt)) {
-      atomicAdd(a.out.sums, sb);
-      atomicAdd(a.out.sums + 1, stt);
+    if ((threadIdx.x & 31) == 0) {
+      part[0][threadIdx.x >> 5] = sb;
+      part[1][threadIdx.x >> 5] = stt;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      const unsigned long long v = part[threadIdx.x][0] + part[threadIdx.x][1] +
+                                   part[threadIdx.x][2] + part[threadIdx.x][3];
+      if (v) atomicAdd(a.out.sums + threadIdx.x, v);
     }
   }
 }
