@@ -25,6 +25,7 @@ namespace hrpp {
 #define HRPP_NODE_F64 1
 #endif
 
+
 #if HRPP_NODE_F64
 struct __align__(16) DNode {  // 64 B: four 16-B loads
   double lo[3], hi[3];
@@ -86,11 +87,13 @@ __host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b
 constexpr double kDetEps = 1e-9;          // hrpp/kernels.py:20
 constexpr double kWrongClosestEps = 1e-9; // hrpp/tracer.py:52
 
+// Traversal result.  The barycentrics (u, v) of the hit are not carried
+// through the loop (4 registers): hit_uv recomputes them from the winning
+// slot with the same arithmetic when an output needs them.
 struct Hit {
   bool found;
   double t;
   int32_t slot, leaf;
-  double u, v;
   int32_t boxes, tris;  // per-ray counts are small; widened when stored
 };
 
@@ -201,6 +204,7 @@ __device__ __forceinline__ Ray make_ray(const float* __restrict__ O, const float
   Ray r;
   r.ox = O[3 * i]; r.oy = O[3 * i + 1]; r.oz = O[3 * i + 2];
   r.dx = D[3 * i]; r.dy = D[3 * i + 1]; r.dz = D[3 * i + 2];
+
   r.ivx = recip(r.dx); r.ivy = recip(r.dy); r.ivz = recip(r.dz);
   r.tmin = tmin[i];
   r.tmax = tmax[i];
@@ -233,8 +237,6 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   h.t = CLOSEST ? r.tmax : 0.0;
   h.slot = -1;
   h.leaf = -1;
-  h.u = 0.0;
-  h.v = 0.0;
   h.boxes = 0;
   h.tris = 0;
   for (;;) {
@@ -247,8 +249,9 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         const int axis = (uint32_t)b >> 30;
         const int32_t right = b & 0x3FFFFFFF;
         const double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
-        stack[top++] = dval >= 0.0 ? right : a;  // far
-        nd = dval >= 0.0 ? a : right;            // near, visited next
+        const int32_t far = dval >= 0.0 ? right : a;
+        stack[top++] = far;
+        nd = dval >= 0.0 ? a : right;  // near, visited next
         continue;
       }
       const int32_t f = ~a, e = f + b;
@@ -258,11 +261,11 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         if (tri_test(tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) && t >= r.tmin &&
             t <= r.tmax) {
           if (!CLOSEST) {
-            h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+            h.found = true; h.t = t; h.slot = k; h.leaf = nd;
             return h;
           }
           if (!h.found || t < h.t) {
-            h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+            h.found = true; h.t = t; h.slot = k; h.leaf = nd;
           }
         }
       }
@@ -289,7 +292,17 @@ __device__ __forceinline__ void fold_entry(Hit& acc, const Hit& r) {
   acc.tris += r.tris;
   if (r.found && (!acc.found || (CLOSEST && r.t < acc.t))) {
     acc.found = true; acc.t = r.t; acc.slot = r.slot; acc.leaf = r.leaf;
-    acc.u = r.u; acc.v = r.v;
+  }
+}
+
+// (u, v) of h's triangle: the reference's values, recomputed (0, 0 on a miss).
+__device__ __forceinline__ void hit_uv(const DTri* __restrict__ tris, const Ray& r, const Hit& h,
+                                       double& u, double& v) {
+  u = 0.0;
+  v = 0.0;
+  if (h.found) {
+    double t;
+    tri_test(tris, h.slot, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v);
   }
 }
 
@@ -297,7 +310,7 @@ __device__ __forceinline__ Hit empty_entry_result(bool closest) {
   Hit h;
   h.found = false;
   h.t = closest ? __longlong_as_double(0x7ff0000000000000LL) : 0.0;
-  h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0; h.boxes = 0; h.tris = 0;
+  h.slot = -1; h.leaf = -1; h.boxes = 0; h.tris = 0;
   return h;
 }
 

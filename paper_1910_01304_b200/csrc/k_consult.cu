@@ -110,8 +110,6 @@ __device__ __forceinline__ void load_state(const ConsultArgs& a, int32_t pos, Hi
   acc.t = s.t;
   acc.slot = s.slot;
   acc.leaf = s.leaf;
-  acc.u = 0.0;
-  acc.v = 0.0;
   acc.boxes = s.boxes;
   acc.tris = s.tris;
   applied = s.applied;
@@ -286,6 +284,7 @@ __global__ void k_first_append(ConsultArgs a, int64_t n) {
     const int32_t s = a.seg_of_ray[i];
     const int32_t ex_len = a.seg_exlen[s];
     if (ex_len > 0 && a.state[i].found) continue;  // TP against the wave-start entry
+    if (a.f_known && !a.f_known[i]) continue;  // (live) no full result: never a first append
     if (!a.f_found[i]) continue;
     if (!in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[i]]))
       atomicMin(a.seg_f1 + s, (int32_t)i);
@@ -581,7 +580,8 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
   if (valid) get_state<CLOSEST>(a, idx, ex_len, acc, applied);
   int32_t L = ex_len + napp;
   int32_t cnode = -1;
-  if (valid && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
+  // a TP's full result may never have been computed (live): read only known ones
+  if (valid && (!LIVE || a.f_known[idx]) && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
   bool inL = false;
   if (valid)
     for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;

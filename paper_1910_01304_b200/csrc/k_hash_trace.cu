@@ -157,8 +157,12 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     if (o.t) o.t[i] = h.t;
     if (o.slot) o.slot[i] = h.slot;
     if (o.leaf) o.leaf[i] = h.leaf;
-    if (CLOSEST && o.u) o.u[i] = h.u;
-    if (CLOSEST && o.v) o.v[i] = h.v;
+    if (CLOSEST && (o.u || o.v)) {
+      double u, v;
+      hit_uv(a.tris, r, h, u, v);
+      if (o.u) o.u[i] = u;
+      if (o.v) o.v[i] = v;
+    }
     if (o.box) o.box[i] = h.boxes;
     if (o.tri) o.tri[i] = h.tris;
     if (o.vis) o.vis[i] = h.boxes;  // visited == box_tests (kernels.py:115-116)
@@ -198,13 +202,18 @@ constexpr int kRefillBelow = HRPP_REFILL_BELOW;
 int g_trace_persistent = 0;
 
 template <bool CLOSEST>
-__device__ __forceinline__ void store_hit(const TraceOut& o, int64_t i, const Hit& h) {
+__device__ __forceinline__ void store_hit(const TraceOut& o, const DTri* tris, const Ray& r,
+                                          int64_t i, const Hit& h) {
   if (o.found) o.found[i] = h.found;
   if (o.t) o.t[i] = h.t;
   if (o.slot) o.slot[i] = h.slot;
   if (o.leaf) o.leaf[i] = h.leaf;
-  if (CLOSEST && o.u) o.u[i] = h.u;
-  if (CLOSEST && o.v) o.v[i] = h.v;
+  if (CLOSEST && (o.u || o.v)) {
+    double u, v;
+    hit_uv(tris, r, h, u, v);
+    if (o.u) o.u[i] = u;
+    if (o.v) o.v[i] = v;
+  }
   if (o.box) o.box[i] = h.boxes;
   if (o.tri) o.tri[i] = h.tris;
   if (o.vis) o.vis[i] = h.boxes;
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(128, HRPP_PERSIST_MINB) k_trace_persist(TraceA
   int top = 0;
   int32_t nd = -1;  // next node to box-test; -1 = lane idle
   Hit h;
-  h.found = false; h.t = 0.0; h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0;
+  h.found = false; h.t = 0.0; h.slot = -1; h.leaf = -1;
   h.boxes = 0; h.tris = 0;
   Ray r{};
   int64_t cur = -1;
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(128, HRPP_PERSIST_MINB) k_trace_persist(TraceA
           top = 0;
           h.found = false;
           h.t = CLOSEST ? r.tmax : 0.0;
-          h.slot = -1; h.leaf = -1; h.u = 0.0; h.v = 0.0; h.boxes = 0; h.tris = 0;
+          h.slot = -1; h.leaf = -1; h.boxes = 0; h.tris = 0;
         }
         const int took = __popc(idle) < avail ? __popc(idle) : avail;
         c_lo += took;
@@ -290,12 +299,12 @@ __global__ void __launch_bounds__(128, HRPP_PERSIST_MINB) k_trace_persist(TraceA
             if (tri_test(a.tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) &&
                 t >= r.tmin && t <= r.tmax) {
               if (!CLOSEST) {
-                h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+                h.found = true; h.t = t; h.slot = k; h.leaf = nd;
                 stop = true;
                 break;
               }
               if (!h.found || t < h.t) {
-                h.found = true; h.t = t; h.slot = k; h.leaf = nd; h.u = u; h.v = v;
+                h.found = true; h.t = t; h.slot = k; h.leaf = nd;
               }
             }
           }
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(128, HRPP_PERSIST_MINB) k_trace_persist(TraceA
         nd = top > 0 ? stack[--top] : -1;
       }
       if (nd < 0) {
-        store_hit<CLOSEST>(a.out, cur, h);
+        store_hit<CLOSEST>(a.out, a.tris, r, cur, h);
         sb += h.boxes;
         stt += h.tris;
         cur = -1;

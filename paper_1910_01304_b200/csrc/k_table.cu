@@ -784,8 +784,12 @@ __global__ void __launch_bounds__(128) k_predict(PredictArgs a) {
   if (a.t) a.t[i] = acc.t;
   if (a.slot) a.slot[i] = acc.slot;
   if (a.leaf) a.leaf[i] = acc.leaf;
-  if (a.u) a.u[i] = acc.u;
-  if (a.v) a.v[i] = acc.v;
+  if (a.u || a.v) {
+    double u = 0.0, v = 0.0;
+    if (e >= 0) hit_uv(a.tris, make_ray(a.O, a.D, a.tmin, a.tmax, i), acc, u, v);
+    if (a.u) a.u[i] = u;
+    if (a.v) a.v[i] = v;
+  }
   if (a.box) a.box[i] = acc.boxes;
   if (a.tri) a.tri[i] = acc.tris;
   if (a.vis) a.vis[i] = acc.boxes;
