@@ -395,8 +395,18 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
   }
   int stack = choose_stack(height);
   CHECK_ARG(stack > 0, "BVH deeper than the 512-entry traversal stack");
+  // slot -> leaf (the traversal reads a hit's leaf from its triangle record)
+  std::vector<int32_t> leaf_of(n_tris > 0 ? n_tris : 1, -1);
+  for (int64_t nd = 0; nd < n_nodes; nd++) {
+    if (left[nd] >= 0) continue;
+    for (int64_t k = first[nd]; k < (int64_t)first[nd] + count[nd]; k++) {
+      CHECK_ARG(leaf_of[k] < 0, "leaf slot ranges overlap");
+      leaf_of[k] = (int32_t)nd;
+    }
+  }
   std::vector<DTri> ht(n_tris > 0 ? n_tris : 1);
-  for (int64_t k = 0; k < n_tris; k++) pack_tri(ht[k], tv0 + 3 * k, tv1 + 3 * k, tv2 + 3 * k);
+  for (int64_t k = 0; k < n_tris; k++)
+    pack_tri(ht[k], tv0 + 3 * k, tv1 + 3 * k, tv2 + 3 * k, leaf_of[k]);
   auto* h = new hrpp_bvh_s();
   h->device = device;
   h->n_nodes = n_nodes;

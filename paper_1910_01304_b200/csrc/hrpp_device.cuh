@@ -34,7 +34,8 @@ struct __align__(16) DNode {  // 64 B: four 16-B loads
 };
 struct __align__(16) DTri {  // 80 B: five 16-B loads
   double v[9];
-  double pad;
+  int32_t leaf;  // the leaf node whose slot range holds this slot (-1: none)
+  int32_t pad;
 };
 #else
 struct __align__(16) DNode {  // 32 B: two 16-B loads
@@ -69,18 +70,30 @@ __host__ __device__ inline void pack_node(DNode& d, const float* lo, const float
 #endif
 }
 
-__host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b, const float* c) {
+__host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b, const float* c,
+                                         int32_t leaf) {
 #if HRPP_NODE_F64
   for (int k = 0; k < 3; k++) {
     t.v[k] = a[k];
     t.v[3 + k] = b[k];
     t.v[6 + k] = c[k];
   }
-  t.pad = 0.0;
+  t.leaf = leaf;
+  t.pad = 0;
 #else
   t.p0 = make_float4(a[0], a[1], a[2], b[0]);
   t.p1 = make_float4(b[1], b[2], c[0], c[1]);
-  t.p2 = make_float4(c[2], 0.f, 0.f, 0.f);
+  t.p2 = make_float4(c[2], __int_as_float(leaf), 0.f, 0.f);
+#endif
+}
+
+// The leaf node holding slot k (leaf slot ranges are disjoint, checked when
+// the BVH is created), so the traversal loop need not carry it.
+__device__ __forceinline__ int32_t slot_leaf(const DTri* __restrict__ tris, int32_t k) {
+#if HRPP_NODE_F64
+  return __ldg(&tris[k].leaf);
+#else
+  return __float_as_int(__ldg(&tris[k].p2.y));
 #endif
 }
 
@@ -230,13 +243,16 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   // The reference pushes far then near and pops near next; visiting the near
   // child directly (only far goes to the stack) is the same visit order with
   // one local-memory store and load less per interior node.
+  // Only slot and t live in the loop: found = slot >= 0 and the leaf is
+  // read from the slot's triangle record at the end.
   int top = 0;
   int32_t nd = start;
+  // d[axis] < 0 per axis (bit axis): the near child is the right one
+  const uint32_t dneg = (r.dx >= 0.0 ? 0u : 1u) | (r.dy >= 0.0 ? 0u : 2u) |
+                        (r.dz >= 0.0 ? 0u : 4u);
   Hit h;
-  h.found = false;
   h.t = CLOSEST ? r.tmax : 0.0;
   h.slot = -1;
-  h.leaf = -1;
   h.boxes = 0;
   h.tris = 0;
   for (;;) {
@@ -246,12 +262,11 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
       const int32_t a = nb.a;
       const int32_t b = nb.b;
       if (a >= 0) {
-        const int axis = (uint32_t)b >> 30;
+        const uint32_t axis = (uint32_t)b >> 30;
         const int32_t right = b & 0x3FFFFFFF;
-        const double dval = axis == 1 ? r.dy : (axis == 2 ? r.dz : r.dx);
-        const int32_t far = dval >= 0.0 ? right : a;
-        stack[top++] = far;
-        nd = dval >= 0.0 ? a : right;  // near, visited next
+        const bool go_right = (dneg >> axis) & 1u;
+        stack[top++] = go_right ? a : right;  // far
+        nd = go_right ? right : a;             // near, visited next
         continue;
       }
       const int32_t f = ~a, e = f + b;
@@ -261,18 +276,24 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         if (tri_test(tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) && t >= r.tmin &&
             t <= r.tmax) {
           if (!CLOSEST) {
-            h.found = true; h.t = t; h.slot = k; h.leaf = nd;
-            return h;
+            h.t = t;
+            h.slot = k;
+            top = 0;
+            break;
           }
-          if (!h.found || t < h.t) {
-            h.found = true; h.t = t; h.slot = k; h.leaf = nd;
+          if (h.slot < 0 || t < h.t) {
+            h.t = t;
+            h.slot = k;
           }
         }
       }
+      if (!CLOSEST && h.slot >= 0) break;
     }
     if (top == 0) break;
     nd = stack[--top];
   }
+  h.found = h.slot >= 0;
+  h.leaf = h.found ? slot_leaf(tris, h.slot) : -1;
   return h;
 }
 
