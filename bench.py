@@ -363,58 +363,74 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        h_in, h_out, d_in, d_out = [], [], [], []
+        h_in, h_out = [], []
         h2d = d2h = 0
         for w in my:
             n = w[3].shape[0]
             h_in.append([pin(a) for a in w[3:]])
-            d_in.append([torch.empty_like(t, device=dev) for t in h_in[-1]])
-            mk = lambda dt, d=None: torch.empty(n, dtype=dt, device=d)  # noqa: E731
-            h_out.append({"found": mk(torch.bool).pin_memory(),
-                          "t": mk(torch.float64).pin_memory(),
-                          "slot": mk(torch.int32).pin_memory(),
-                          "leaf": mk(torch.int32).pin_memory()})
-            d_out.append({k: torch.empty_like(v, device=dev) for k, v in h_out[-1].items()})
+            mk = lambda dt: torch.empty(n, dtype=dt).pin_memory()  # noqa: E731
+            h_out.append({"found": mk(torch.bool), "t": mk(torch.float64),
+                          "slot": mk(torch.int32), "leaf": mk(torch.int32)})
             h2d += sum(t.numel() * t.element_size() for t in h_in[-1])
             d2h += sum(t.numel() * t.element_size() for t in h_out[-1].values())
+        # device buffers double-buffered by frame parity, so the uploads of
+        # frame f+1 run while frame f computes
+        d_in = [[[torch.empty_like(t, device=dev) for t in h] for h in h_in] for _ in range(2)]
+        d_out = [[{k: torch.empty_like(v, device=dev) for k, v in h.items()} for h in h_out]
+                 for _ in range(2)]
         copy = torch.cuda.Stream(device=dev)   # uploads
         copy_back = torch.cuda.Stream(device=dev)  # downloads (the other copy engine)
+        W = len(my)
 
         def run_e2e(frames):
-            """`frames` frames back to back, one (frame, wave) pipeline: the
-            upload of the next item overlaps the compute of the current one."""
-            items = [(f, j) for f in range(frames) for j in range(len(my))]
-            ev_in = [torch.cuda.Event() for _ in items]
+            """`frames` frames back to back as one (frame, wave) pipeline:
+            uploads run a whole frame ahead on one copy engine, downloads on
+            the other, the waves in order on the compute stream."""
+            items = [(f, j) for f in range(frames) for j in range(W)]
+            ev_up = [torch.cuda.Event() for _ in items]
+            ev_comp = [torch.cuda.Event() for _ in items]
+            ev_down = [torch.cuda.Event() for _ in items]
+
+            skip = os.environ.get("HRPP_E2E_DIAG_SKIP", "")  # diagnosis only: up|down
 
             def upload(i):
-                _, j = items[i]
+                f, j = items[i]
+                if skip == "up" and i >= W:
+                    ev_up[i].record(copy)
+                    return
                 with torch.cuda.stream(copy):
-                    for d_, h_ in zip(d_in[j], h_in[j]):
+                    if i >= 2 * W:  # buffer last read by item i - 2W
+                        copy.wait_event(ev_comp[i - 2 * W])
+                    for d_, h_ in zip(d_in[f % 2][j], h_in[j]):
                         d_.copy_(h_, non_blocking=True)
-                    ev_in[i].record(copy)
+                    ev_up[i].record(copy)
 
-            upload(0)
+            for i in range(min(W, len(items))):
+                upload(i)
             for i, (f, j) in enumerate(items):
                 if j == 0:
                     for t in tables.values():
                         t.clear()
-                if i + 1 < len(items):
-                    upload(i + 1)
-                stream.wait_event(ev_in[i])
-                run_wave(j, "live", *d_in[j], outputs=d_out[j])
-                done = torch.cuda.Event()
-                done.record(stream)
-                copy_back.wait_event(done)
+                if i + W < len(items):
+                    upload(i + W)
+                stream.wait_event(ev_up[i])
+                if i >= 2 * W:  # output buffer last downloaded by item i - 2W
+                    stream.wait_event(ev_down[i - 2 * W])
+                run_wave(j, "live", *d_in[f % 2][j], outputs=d_out[f % 2][j])
+                ev_comp[i].record(stream)
+                copy_back.wait_event(ev_comp[i])
                 with torch.cuda.stream(copy_back):
-                    for k in h_out[j]:
-                        h_out[j][k].copy_(d_out[j][k], non_blocking=True)
+                    if skip != "down":
+                        for k in h_out[j]:
+                            h_out[j][k].copy_(d_out[f % 2][j][k], non_blocking=True)
+                    ev_down[i].record(copy_back)
             copy.synchronize()
             copy_back.synchronize()
 
         run_e2e(1)
         barrier()
         t0w = time.perf_counter()
-        e_steps = max(1, min(args.steps, 3))
+        e_steps = args.steps
         run_e2e(e_steps)
         barrier()
         dt = time.perf_counter() - t0w
@@ -425,8 +441,9 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": round(n_total * e_steps / dt / 1e6, 3), "unit": "Mrays/s",
                "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
                "how": "pinned host inputs -> trace_wave (public API) -> pinned host hits every "
-                      "step; copies on a side stream overlapped with the neighbouring waves' "
-                      "compute (frames back to back); wall clock"}
+                      "step; uploads one frame ahead (double-buffered) and downloads on the two "
+                      "copy engines, overlapped with compute; K frames back to back; wall "
+                      "clock"}
 
     # ---- CPU baseline (oracle port, rank 0, N=1 only) ---------------------------------
     cpu = None

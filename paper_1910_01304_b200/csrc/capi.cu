@@ -231,11 +231,36 @@ static int choose_stack(int height) {
 struct Pinned {
   long long* p = nullptr;
   int get() {
-    if (!p) HRPP_CK(cudaMallocHost(&p, sizeof(long long) * 40));
+    if (!p) HRPP_CK(cudaHostAlloc(&p, sizeof(long long) * 64, cudaHostAllocMapped));
     return 0;
   }
 };
 static thread_local Pinned g_pinned;  // per host thread (see global_ws)
+
+long long* pinned_scratch() { return g_pinned.get() ? nullptr : g_pinned.p; }
+
+__global__ void k_to_host(char* dst, const char* src, int bytes) {
+  for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+__global__ void k_set_i32(int32_t* dst, int32_t v) { *dst = v; }
+__global__ void k_set_i64(long long* dst, long long v) { *dst = v; }
+
+int to_host(void* pinned_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return 0;
+  k_to_host<<<1, 128, 0, st>>>((char*)pinned_dst, (const char*)dev_src, (int)bytes);
+  HRPP_LAUNCHED();
+  return 0;
+}
+int set_i32(int32_t* dst, int32_t v, cudaStream_t st) {
+  k_set_i32<<<1, 1, 0, st>>>(dst, v);
+  HRPP_LAUNCHED();
+  return 0;
+}
+int set_i64(long long* dst, long long v, cudaStream_t st) {
+  k_set_i64<<<1, 1, 0, st>>>(dst, v);
+  HRPP_LAUNCHED();
+  return 0;
+}
 
 }  // namespace hrpp
 
@@ -319,7 +344,7 @@ int hrpp_hash_rays(const float* O, const float* D, int64_t n, int p, uint64_t* k
   HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
   if ((rc = launch_hash(dO, dD, n, p, dk, err, st))) return rc;
   if ((rc = g_pinned.get())) return rc;
-  HRPP_CK(cudaMemcpyAsync(g_pinned.p, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if ((rc = to_host(g_pinned.p, err, sizeof(int), st))) return rc;
   if ((rc = sg.finish())) return rc;
   if (*(int*)g_pinned.p) {
     set_error("non-finite ray component in hash batch");
@@ -342,7 +367,7 @@ int hrpp_hash_floats(const float* f, int64_t n, int p, uint32_t* out, void* stre
   HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
   if ((rc = launch_hash_floats(df, n, p, dout, err, st))) return rc;
   if ((rc = g_pinned.get())) return rc;
-  HRPP_CK(cudaMemcpyAsync(g_pinned.p, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if ((rc = to_host(g_pinned.p, err, sizeof(int), st))) return rc;
   if ((rc = sg.finish())) return rc;
   if (*(int*)g_pinned.p) {
     set_error("cannot hash non-finite float");
@@ -539,12 +564,10 @@ static int read_meta_and_finish(TableDev& t, int* err, cudaStream_t st, Stager& 
                                 unsigned long long* stats_dev) {
   int rc;
   if ((rc = g_pinned.get())) return rc;
-  HRPP_CK(cudaMemcpyAsync(g_pinned.p + 28, t.meta, sizeof(long long) * 4, cudaMemcpyDeviceToHost,
-                          st));
-  HRPP_CK(cudaMemcpyAsync(g_pinned.p + 3, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if ((rc = to_host(g_pinned.p + 28, t.meta, sizeof(long long) * 4, st))) return rc;
+  if ((rc = to_host(g_pinned.p + 3, err, sizeof(int), st))) return rc;
   if (stats_dev)
-    HRPP_CK(cudaMemcpyAsync(g_pinned.p + 4, stats_dev, sizeof(long long) * 16,
-                            cudaMemcpyDeviceToHost, st));
+    if ((rc = to_host(g_pinned.p + 4, stats_dev, sizeof(long long) * 16, st))) return rc;
   if ((rc = sg.finish())) return rc;
   int e = *(int*)(g_pinned.p + 3);
   if (e == 0) {
@@ -751,9 +774,8 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
     if ((rc = read_meta_and_finish(*t, err, st, sg, sdev))) return rc;
   } else {
     if ((rc = g_pinned.get())) return rc;
-    HRPP_CK(cudaMemcpyAsync(g_pinned.p + 3, err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    HRPP_CK(cudaMemcpyAsync(g_pinned.p + 4, sdev, sizeof(long long) * 16, cudaMemcpyDeviceToHost,
-                            st));
+    if ((rc = to_host(g_pinned.p + 3, err, sizeof(int), st))) return rc;
+    if ((rc = to_host(g_pinned.p + 4, sdev, sizeof(long long) * 16, st))) return rc;
     if ((rc = sg.finish())) return rc;
   }
   const int e = *(int*)(g_pinned.p + 3);

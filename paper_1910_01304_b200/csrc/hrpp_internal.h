@@ -194,6 +194,16 @@ int predict_batch(const BvhDev& b, TableDev& t, const uint64_t* keys, const floa
                   int8_t* cls, double* tt, int32_t* slot, int32_t* leaf, double* u, double* v,
                   int64_t* box, int64_t* tri, int64_t* vis, int64_t* est, cudaStream_t st);
 
+// Small device->host reads without a copy engine: a one-block kernel stores
+// into this host thread's pinned buffer (UVA-mapped), then the caller syncs
+// the stream.  Large user copies keep the DMA engines to themselves, so a
+// 4-byte readback never queues behind a 100-MB upload or download.
+long long* pinned_scratch();  // 64 entries; [32, 64) free for kernels' use
+int to_host(void* pinned_dst, const void* dev_src, size_t bytes, cudaStream_t st);
+// Small host->device values as kernel arguments (no copy engine either).
+int set_i32(int32_t* dst, int32_t v, cudaStream_t st);
+int set_i64(long long* dst, long long v, cudaStream_t st);
+
 extern int g_live_rounds;
 
 inline int grid_for(int64_t n, int block, int max_blocks) {

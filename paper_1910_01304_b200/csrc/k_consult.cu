@@ -26,7 +26,9 @@
 // rounds one speculative round traces every unresolved ray.  Either way the
 // results are exact: speculation only costs traversals.
 #include <cub/cub.cuh>
+#include <cstring>
 
+#include "../../include/hrpp_b200.h"
 #include "hrpp_internal.h"
 
 namespace hrpp {
@@ -752,8 +754,11 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds);
   HRPP_LAUNCHED();
   int hb[9];
-  HRPP_CK(cudaMemcpyAsync(hb, bounds, sizeof(int) * 9, cudaMemcpyDeviceToHost, st));
+  long long* pin = pinned_scratch();
+  if (!pin) return HRPP_CUDA;
+  if ((rc = to_host(pin + 40, bounds, sizeof(int) * 9, st))) return rc;
   HRPP_CK(cudaStreamSynchronize(st));
+  memcpy(hb, pin + 40, sizeof(int) * 9);
   auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
 #define HRPP_GROUP(K, GS)                                                                      \
   if (cnt(K) > 0) {                                                                            \
@@ -773,7 +778,7 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
     int* dcount;
     if ((rc = ws.get("rg_lcount", 1, &dcount))) return rc;
     const int c7 = cnt(7);
-    HRPP_CK(cudaMemcpyAsync(dcount, &c7, sizeof(int), cudaMemcpyHostToDevice, st));
+    if ((rc = set_i32(dcount, c7, st))) return rc;
     k_replay_long<CLOSEST, LIVE, STACK><<<(c7 * 32 + 127) / 128, 128, 0, st>>>(
         a, ids_sorted + hb[7], dcount);
     HRPP_LAUNCHED();
@@ -844,9 +849,11 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st))) return rc;
   // new entries <= key segments: read the segment count once so the hash
   // index stays sized to the table (L2-resident for c1-c3 tables), not to the wave
-  int nsegs_h = 0;
-  HRPP_CK(cudaMemcpyAsync(&nsegs_h, seg.nsegs, sizeof(int), cudaMemcpyDeviceToHost, st));
+  long long* pin = pinned_scratch();
+  if (!pin) return HRPP_CUDA;
+  if ((rc = to_host(pin + 32, seg.nsegs, sizeof(int), st))) return rc;
   HRPP_CK(cudaStreamSynchronize(st));
+  int nsegs_h = *(volatile int*)(pin + 32);
   if ((rc = t.reserve(nsegs_h, n, st))) return rc;
   Workspace& ws = t.ws;
   ConsultArgs a{};

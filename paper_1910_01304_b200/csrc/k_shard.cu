@@ -76,9 +76,13 @@ extern "C" int hrpp_partition_by_owner(const uint64_t* keys, int64_t n, int worl
                                               st));
     }
   }
-  unsigned long long h[256];
-  HRPP_CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long) * world, cudaMemcpyDeviceToHost, st));
-  HRPP_CK(cudaStreamSynchronize(st));
-  for (int k = 0; k < world; k++) counts[k] = (int64_t)h[k];
+  long long* pin = pinned_scratch();
+  if (!pin) return HRPP_CUDA;
+  for (int k0 = 0; k0 < world; k0 += 32) {  // 32 counters per readback
+    const int m2 = world - k0 < 32 ? world - k0 : 32;
+    if ((rc = to_host(pin + 32, cnt + k0, sizeof(unsigned long long) * m2, st))) return rc;
+    HRPP_CK(cudaStreamSynchronize(st));
+    for (int k = 0; k < m2; k++) counts[k0 + k] = ((volatile long long*)pin)[32 + k];
+  }
   return HRPP_OK;
 }

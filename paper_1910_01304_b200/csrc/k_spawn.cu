@@ -282,9 +282,10 @@ extern "C" int hrpp_spawn(hrpp_bvh_t bvh, const float* O, const float* D, const 
   a.b1 = b1;
   k_spawn<<<grid_for(n, 128, num_sms() * 16), 128, 0, st>>>(a);
   HRPP_LAUNCHED();
-  int h = 0;
-  HRPP_CK(cudaMemcpyAsync(&h, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  long long* pin = pinned_scratch();
+  if (!pin) return HRPP_CUDA;
+  if ((rc = to_host(pin + 32, cnt, sizeof(int), st))) return rc;
   HRPP_CK(cudaStreamSynchronize(st));
-  *count_out = h;
+  *count_out = *(volatile int*)(pin + 32);
   return HRPP_OK;
 }

@@ -309,9 +309,7 @@ int TableDev::reserve(int64_t extra_e, int64_t extra, cudaStream_t st) {
     arena = na;
     arena_cap = nc;
     arena_used = stored;
-    long long used = stored;
-    HRPP_CK(cudaMemcpyAsync(meta + 2, &used, sizeof(long long), cudaMemcpyHostToDevice, st));
-    HRPP_CK(cudaStreamSynchronize(st));
+    if ((rc = set_i64(meta + 2, stored, st))) return rc;
   }
   return 0;
 }
