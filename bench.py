@@ -123,6 +123,9 @@ def shard(wave, rank, world):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock and clock-event reasons sampled during the timed region: NVML
+    every 2 ms from a thread (a timed region of a few frames is < 100 ms, too
+    short for nvidia-smi's polling); nvidia-smi -lms as the fallback."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -131,12 +134,38 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self.device = device
+        self.nv = None
+        self.stop = threading.Event()
 
     def __enter__(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = (("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+                    ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+                    ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+                    ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap))
+
+            def poll():
+                while not self.stop.is_set():
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    flags = ["Active" if r & b else "Not Active" for _, b in bits]
+                    self.lines.append(", ".join([str(sm), str(mx), "0", hex(r)] + flags))
+                    time.sleep(0.002)
+
+            self.nv = nv
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nv = None
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -149,6 +178,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1)
         if self.proc is not None:
             self.proc.terminate()
             try:
