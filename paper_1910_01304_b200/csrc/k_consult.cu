@@ -147,6 +147,18 @@ struct Tally {
   long long tp = 0, fp = 0, neg = 0, ob = 0, ot = 0, sk = 0, est = 0, wr = 0, bb = 0, bt = 0;
 };
 
+// Add a warp's tallies into the wave counters (for kernels whose warps
+// finish at very different times: no block barrier holds finished warps).
+__device__ __forceinline__ void flush_tally_warp(const Tally& c, unsigned long long* stats) {
+  const long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
+  const int slot[10] = {S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG};
+#pragma unroll
+  for (int k = 0; k < 10; k++) {
+    const long long w = warp_sum(v[k]);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(stats + slot[k], (unsigned long long)w);
+  }
+}
+
 // Add a block's tallies into the wave counters: warp sums, then one atomic
 // per counter per block (per-warp atomics on 10 shared addresses serialised
 // in L2).  Every thread of the block must call it.
@@ -531,7 +543,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_short(ConsultA
     const int32_t cur = a.seg_cursor[s];
     if (cur < end && end - beg <= short_len) seg_thread<CLOSEST, LIVE, STACK>(a, c, s, beg, end, cur);
   }
-  flush_tally(c, a.stats);
+  flush_tally_warp(c, a.stats);
 }
 
 // Long segments: one warp per segment of the compacted list.
@@ -545,7 +557,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_long(ConsultAr
   const int m = *count;
   Tally c;
   for (int k = w; k < m; k += nw) seg_warp<CLOSEST, LIVE, STACK>(a, c, list[k], lane);
-  flush_tally(c, a.stats);
+  flush_tally_warp(c, a.stats);
 }
 
 // Grouped single-tile replay: a group of G lanes replays one key segment
@@ -625,7 +637,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
     a.seg_napp[s] = napp;
     a.seg_cursor[s] = end;
   }
-  flush_tally(c, a.stats);
+  flush_tally_warp(c, a.stats);
 }
 
 // Replay length class of every segment (rays left): 0 done, 1..6 for
