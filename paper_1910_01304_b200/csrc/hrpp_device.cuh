@@ -24,6 +24,9 @@ namespace hrpp {
 #ifndef HRPP_NODE_F64
 #define HRPP_NODE_F64 1
 #endif
+#ifndef HRPP_OPAQUE_SIGNS
+#define HRPP_OPAQUE_SIGNS 1
+#endif
 
 
 #if HRPP_NODE_F64
@@ -162,6 +165,30 @@ __device__ __forceinline__ bool box_hit(const NodeBox& n, double ox, double oy, 
   return tn <= tf;
 }
 
+// box_hit with the swap decisions (inv < 0 per axis) precomputed per ray as
+// bits of `ivneg`: integer tests instead of three float64 compares per box.
+__device__ __forceinline__ bool box_hit_s(const NodeBox& n, double ox, double oy, double oz,
+                                          double ivx, double ivy, double ivz, uint32_t ivneg,
+                                          double t0, double t1) {
+  double tn = t0, tf = t1, a, b, s;
+  a = (n.lx - ox) * ivx;
+  b = (n.hx - ox) * ivx;
+  if (ivneg & 1u) { s = a; a = b; b = s; }
+  if (a > tn) tn = a;
+  if (b < tf) tf = b;
+  a = (n.ly - oy) * ivy;
+  b = (n.hy - oy) * ivy;
+  if (ivneg & 2u) { s = a; a = b; b = s; }
+  if (a > tn) tn = a;
+  if (b < tf) tf = b;
+  a = (n.lz - oz) * ivz;
+  b = (n.hz - oz) * ivz;
+  if (ivneg & 4u) { s = a; a = b; b = s; }
+  if (a > tn) tn = a;
+  if (b < tf) tf = b;
+  return tn <= tf;
+}
+
 // Triangle vertices widened to float64 (exact).
 __device__ __forceinline__ void load_tri(const DTri* __restrict__ tris, int32_t k, double v[9]) {
 #if HRPP_NODE_F64
@@ -250,15 +277,24 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   // d[axis] < 0 per axis (bit axis): the near child is the right one
   const uint32_t dneg = (r.dx >= 0.0 ? 0u : 1u) | (r.dy >= 0.0 ? 0u : 2u) |
                         (r.dz >= 0.0 ? 0u : 4u);
+  uint32_t ivneg = (r.ivx < 0.0 ? 1u : 0u) | (r.ivy < 0.0 ? 2u : 0u) |
+                   (r.ivz < 0.0 ? 4u : 0u);
+#if HRPP_OPAQUE_SIGNS
+  asm volatile("mov.u32 %0, %0;" : "+r"(ivneg));  // keep the bits, not 3 float64 compares
+#endif
+  // h.t starts at tmax for both kinds: the closest-hit box interval is
+  // [tmin, best t] and a hit needs t <= tmax before the first hit and
+  // t < best t after it; an any-hit ray's interval stays [tmin, tmax] until
+  // its first hit ends the traversal.  So tmax itself is not live here.
   Hit h;
-  h.t = CLOSEST ? r.tmax : 0.0;
+  h.t = r.tmax;
   h.slot = -1;
   h.boxes = 0;
   h.tris = 0;
   for (;;) {
     h.boxes++;
     const NodeBox nb = load_node(nodes, nd);
-    if (box_hit(nb, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, r.tmin, CLOSEST ? h.t : r.tmax)) {
+    if (box_hit_s(nb, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, ivneg, r.tmin, h.t)) {
       const int32_t a = nb.a;
       const int32_t b = nb.b;
       if (a >= 0) {
@@ -274,16 +310,12 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         double t, u, v;
         h.tris++;
         if (tri_test(tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) && t >= r.tmin &&
-            t <= r.tmax) {
+            (h.slot < 0 ? t <= h.t : t < h.t)) {
+          h.t = t;
+          h.slot = k;
           if (!CLOSEST) {
-            h.t = t;
-            h.slot = k;
             top = 0;
             break;
-          }
-          if (h.slot < 0 || t < h.t) {
-            h.t = t;
-            h.slot = k;
           }
         }
       }
@@ -293,6 +325,7 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
     nd = stack[--top];
   }
   h.found = h.slot >= 0;
+  if (!CLOSEST && !h.found) h.t = 0.0;  // trace_any's miss (hrpp/kernels.py:206)
   h.leaf = h.found ? slot_leaf(tris, h.slot) : -1;
   return h;
 }
