@@ -56,7 +56,6 @@ struct Builder {
 
     double best_cost = std::numeric_limits<double>::infinity();
     int best_ax = -1, best_k = -1;
-    std::vector<int> best_bins, bins(n);
     if (!median) {
       for (int ax = 0; ax < 3; ax++) {
         if (ext[ax] <= 0.0) continue;
@@ -72,7 +71,6 @@ struct Builder {
           int64_t i = idx[j];
           int64_t b = (int64_t)((cent[3 * i + ax] - cmin[ax]) * scale);
           if (b > kBins - 1) b = kBins - 1;
-          bins[j] = (int)b;
           counts[b]++;
           for (int a = 0; a < 3; a++) {
             double lo = tmin[3 * i + a], hi = tmax[3 * i + a];
@@ -106,7 +104,6 @@ struct Builder {
             best_cost = cost;
             best_ax = ax;
             best_k = k;
-            best_bins = bins;
           }
         }
       }
@@ -130,7 +127,14 @@ struct Builder {
     L.clear();
     R.clear();
     if (improving) {
-      for (int64_t j = 0; j < n; j++) (best_bins[j] <= best_k ? L : R).push_back(idx[j]);
+      // the winning axis's bins, recomputed with the same arithmetic
+      const double scale = kBins / ext[best_ax];
+      for (int64_t j = 0; j < n; j++) {
+        const int64_t i = idx[j];
+        int64_t b = (int64_t)((cent[3 * i + best_ax] - cmin[best_ax]) * scale);
+        if (b > kBins - 1) b = kBins - 1;
+        (b <= best_k ? L : R).push_back(i);
+      }
       *axis_out = best_ax;
       return true;
     }
