@@ -14,6 +14,7 @@
 // is IEEE round-to-nearest, so results are bit-identical to the reference.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 namespace hrpp {
@@ -27,6 +28,7 @@ namespace hrpp {
 #ifndef HRPP_OPAQUE_SIGNS
 #define HRPP_OPAQUE_SIGNS 1
 #endif
+
 
 
 #if HRPP_NODE_F64
@@ -86,7 +88,9 @@ __host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b
 #else
   t.p0 = make_float4(a[0], a[1], a[2], b[0]);
   t.p1 = make_float4(b[1], b[2], c[0], c[1]);
-  t.p2 = make_float4(c[2], __int_as_float(leaf), 0.f, 0.f);
+  float leaf_bits;
+  memcpy(&leaf_bits, &leaf, sizeof(float));
+  t.p2 = make_float4(c[2], leaf_bits, 0.f, 0.f);
 #endif
 }
 
