@@ -605,33 +605,38 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
     if (applied < L && (CLOSEST || !acc.found))
       catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
   }
+  // Step from append to append: the rays before the next ray that grows the
+  // entry see a constant list, so they are classified together (TP, or
+  // FP/NEG without a new node); only an append changes the later rays.
   int cur_l = 0;
   for (;;) {
-    const bool need = valid && gl >= cur_l && (L == 0 || !acc.found);
-    const unsigned m = __ballot_sync(kFull, need) & gmask;
+    const bool pend = valid && gl >= cur_l;
+    const bool nontp = pend && (L == 0 || !acc.found);
+    const bool grows = nontp && cnode >= 0 && !inL;
+    const unsigned m = __ballot_sync(kFull, grows) & gmask;
     const int f = m ? __ffs(m) - 1 - gbase : G;
-    if (valid && gl >= cur_l && gl < f) commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+    if (pend && gl < f) {
+      if (nontp) commit_miss<LIVE>(a, c, idx, acc, L == 0);
+      else commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+    }
     if (!__any_sync(kFull, f < G)) break;
     const int src = f < G ? gbase + f : lane;
     const int32_t cf = __shfl_sync(kFull, cnode, src);
-    const bool inLf = __shfl_sync(kFull, inL, src);
     const int32_t rf = __shfl_sync(kFull, idx, src);
-    const bool grow = f < G && cf >= 0 && !inLf;
     if (f < G && gl == f) commit_miss<LIVE>(a, c, idx, acc, L == 0);
-    if (grow && gl == 0) {  // record(key, anc[leaf]) grows the entry
+    if (f < G && gl == 0) {  // record(key, anc[leaf]) grows the entry
       app[napp] = cf;
       a.app_ray[beg + napp] = rf;
     }
     __syncwarp();
-    if (grow) {
+    if (f < G) {
       napp++;
       L++;
       inL |= cnode == cf;
       if (valid && gl > f && (CLOSEST || !acc.found))
         catch_up<CLOSEST, STACK>(a, r, acc, L - 1, L, ex_off, ex_len, app);
     }
-    if (f < G) cur_l = f + 1;
-    else cur_l = G;
+    cur_l = f < G ? f + 1 : G;
   }
   if (gvalid && gl == 0) {
     a.seg_napp[s] = napp;
@@ -640,8 +645,97 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
   flush_tally_warp(c, a.stats);
 }
 
+// Very long key segments (coarse hashes: ~10k rays per key at p = 3) would
+// leave the GPU nearly idle with one warp each, so a block of kBlockReplay
+// threads replays one of them in tiles of kBlockReplay consecutive rays:
+// seg_warp's loop with a block-wide "first non-TP ray" (shared-memory
+// atomicMin between barriers).  Same order, same appends, same results.
+constexpr int kBlockReplay = 256;
+constexpr int kBlockReplayMin = 1024;
+
+template <bool CLOSEST, bool LIVE, int STACK, int BS>
+__global__ void __launch_bounds__(BS) k_replay_block(ConsultArgs a, const int32_t* list,
+                                                     int count) {
+  if (*a.err) return;
+  __shared__ int s_f;
+  __shared__ int32_t s_cf, s_rf;
+  const int tid = threadIdx.x;
+  Tally c;
+  for (int k = blockIdx.x; k < count; k += gridDim.x) {
+    const int s = list[k];
+    const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
+    int32_t tb = a.seg_cursor[s];
+    int32_t napp = a.seg_napp[s];
+    const int64_t ex_off = a.seg_exoff[s];
+    const int32_t ex_len = a.seg_exlen[s];
+    int32_t* app = a.app + beg;
+    while (tb < end) {
+      const int32_t pos = tb + tid;
+      const bool valid = pos < end;
+      const int32_t idx = valid ? a.sidx[pos] : 0;
+      Hit acc = empty_entry_result(CLOSEST);
+      int32_t applied = 0;
+      if (valid) get_state<CLOSEST>(a, idx, ex_len, acc, applied);
+      int32_t L = ex_len + napp;
+      int32_t cnode = -1;
+      if (valid && (!LIVE || a.f_known[idx]) && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
+      bool inL = false;
+      if (cnode >= 0)
+        for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
+      Ray r{};
+      if (valid) {
+        r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
+        if (applied < L && (CLOSEST || !acc.found))
+          catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+      }
+      // append to append, as in k_replay_group
+      int cursor = 0;
+      for (;;) {
+        const bool pend = valid && tid >= cursor;
+        const bool nontp = pend && (L == 0 || !acc.found);
+        const bool grows = nontp && cnode >= 0 && !inL;
+        if (tid == 0) s_f = BS;
+        __syncthreads();
+        if (grows) atomicMin(&s_f, tid);
+        __syncthreads();
+        const int f = s_f;
+        if (pend && tid < f) {
+          if (nontp) commit_miss<LIVE>(a, c, idx, acc, L == 0);
+          else commit_tp<CLOSEST, LIVE>(a, c, idx, acc);
+        }
+        if (f == BS) break;
+        if (tid == f) {
+          commit_miss<LIVE>(a, c, idx, acc, L == 0);
+          s_cf = cnode;
+          s_rf = idx;
+        }
+        __syncthreads();
+        const int32_t cf = s_cf;
+        if (tid == 0) {  // record(key, anc[leaf]) grows the entry
+          app[napp] = cf;
+          a.app_ray[beg + napp] = s_rf;
+        }
+        napp++;
+        L++;
+        inL |= cnode == cf;
+        if (valid && tid > f && (CLOSEST || !acc.found))
+          fold_entry<CLOSEST>(acc, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, cf));
+        cursor = f + 1;
+        __syncthreads();  // s_* reused by the next step
+      }
+      tb += BS;
+      __syncthreads();  // app[] written by thread 0 is read by the next tile
+    }
+    if (tid == 0) {
+      a.seg_napp[s] = napp;
+      a.seg_cursor[s] = end;
+    }
+  }
+  flush_tally(c, a.stats);
+}
+
 // Replay length class of every segment (rays left): 0 done, 1..6 for
-// <= 1, 2, 4, 8, 16, 32 rays, 7 longer.
+// <= 1, 2, 4, 8, 16, 32 rays, 7 up to kBlockReplayMin, 8 longer.
 __global__ void k_replay_class(ConsultArgs a, int64_t nseg_cap, uint8_t* cls, int32_t* ids) {
   const int ns = *a.nsegs;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg_cap;
@@ -650,17 +744,17 @@ __global__ void k_replay_class(ConsultArgs a, int64_t nseg_cap, uint8_t* cls, in
     if (s < ns) {
       const int32_t rem = a.seg_start[s + 1] - a.seg_cursor[s];
       k = rem <= 0 ? 0 : rem <= 1 ? 1 : rem <= 2 ? 2 : rem <= 4 ? 3 : rem <= 8 ? 4
-        : rem <= 16 ? 5 : rem <= 32 ? 6 : 7;
+        : rem <= 16 ? 5 : rem <= 32 ? 6 : rem <= kBlockReplayMin ? 7 : 8;
     }
     cls[s] = (uint8_t)k;
     ids[s] = (int32_t)s;
   }
 }
 
-// Start of every class in the class-sorted list (8 entries + end).
+// Start of every class in the class-sorted list (9 entries + end).
 __global__ void k_class_bounds(const uint8_t* sorted_cls, int64_t m, int* bounds) {
   const int k = threadIdx.x;
-  if (k > 8) return;
+  if (k > 9) return;
   int64_t lo = 0, hi = m;  // first position with class >= k
   while (lo < hi) {
     const int64_t mid = (lo + hi) / 2;
@@ -758,19 +852,19 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   k_replay_class<<<grid_for(m, 256, num_sms() * 8), 256, 0, st>>>(a, m, cls, ids);
   HRPP_LAUNCHED();
   size_t b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 3, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 4, st);
   void* tmp;
   if ((rc = ws.get_raw("rg_tmp", b, &tmp))) return rc;
-  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 3,
+  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 4,
                                           st));
   k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds);
   HRPP_LAUNCHED();
-  int hb[9];
+  int hb[10];
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
-  if ((rc = to_host(pin + 40, bounds, sizeof(int) * 9, st))) return rc;
+  if ((rc = to_host(pin + 40, bounds, sizeof(int) * 10, st))) return rc;
   HRPP_CK(cudaStreamSynchronize(st));
-  memcpy(hb, pin + 40, sizeof(int) * 9);
+  memcpy(hb, pin + 40, sizeof(int) * 10);
   auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
 #define HRPP_GROUP(K, GS)                                                                      \
   if (cnt(K) > 0) {                                                                            \
@@ -786,13 +880,14 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   HRPP_GROUP(5, 16)
   HRPP_GROUP(6, 32)
 #undef HRPP_GROUP
-  if (cnt(7) > 0) {
-    int* dcount;
-    if ((rc = ws.get("rg_lcount", 1, &dcount))) return rc;
-    const int c7 = cnt(7);
-    if ((rc = set_i32(dcount, c7, st))) return rc;
-    k_replay_long<CLOSEST, LIVE, STACK><<<(c7 * 32 + 127) / 128, 128, 0, st>>>(
-        a, ids_sorted + hb[7], dcount);
+  if (cnt(7) > 0) {  // long segments: a warp each, 32-ray tiles
+    k_replay_block<CLOSEST, LIVE, STACK, 32><<<cnt(7), 32, 0, st>>>(a, ids_sorted + hb[7],
+                                                                      cnt(7));
+    HRPP_LAUNCHED();
+  }
+  if (cnt(8) > 0) {  // very long segments: a whole block each
+    k_replay_block<CLOSEST, LIVE, STACK, kBlockReplay><<<cnt(8), kBlockReplay, 0, st>>>(
+        a, ids_sorted + hb[8], cnt(8));
     HRPP_LAUNCHED();
   }
   return 0;
