@@ -653,9 +653,13 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
 constexpr int kBlockReplay = 256;
 constexpr int kBlockReplayMin = 1024;
 
+#ifndef HRPP_BLOCK_MINB
+#define HRPP_BLOCK_MINB 2
+#endif
+
 template <bool CLOSEST, bool LIVE, int STACK, int BS>
-__global__ void __launch_bounds__(BS) k_replay_block(ConsultArgs a, const int32_t* list,
-                                                     int count) {
+__global__ void __launch_bounds__(BS, BS == 32 ? 16 : HRPP_BLOCK_MINB)
+    k_replay_block(ConsultArgs a, const int32_t* list, int count) {
   if (*a.err) return;
   __shared__ int s_f;
   __shared__ int32_t s_cf, s_rf;
@@ -732,6 +736,14 @@ __global__ void __launch_bounds__(BS) k_replay_block(ConsultArgs a, const int32_
     }
   }
   flush_tally(c, a.stats);
+}
+
+// Rays left to replay in each listed segment (longest-first scheduling).
+__global__ void k_seg_remaining(ConsultArgs a, const int32_t* list, int m, int32_t* rem) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    const int s = list[k];
+    rem[k] = a.seg_start[s + 1] - a.seg_cursor[s];
+  }
 }
 
 // Replay length class of every segment (rays left): 0 done, 1..6 for
@@ -885,9 +897,23 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
                                                                       cnt(7));
     HRPP_LAUNCHED();
   }
-  if (cnt(8) > 0) {  // very long segments: a whole block each
-    k_replay_block<CLOSEST, LIVE, STACK, kBlockReplay><<<cnt(8), kBlockReplay, 0, st>>>(
-        a, ids_sorted + hb[8], cnt(8));
+  if (cnt(8) > 0) {  // very long segments: a whole block each, longest first
+    const int c8 = cnt(8);
+    int32_t *rem, *rem2, *ids8;
+    if ((rc = ws.get("rg_rem", c8, &rem)) || (rc = ws.get("rg_rem2", c8, &rem2)) ||
+        (rc = ws.get("rg_ids8", c8, &ids8)))
+      return rc;
+    k_seg_remaining<<<grid_for(c8, 256, num_sms() * 4), 256, 0, st>>>(a, ids_sorted + hb[8], c8,
+                                                                       rem);
+    HRPP_LAUNCHED();
+    size_t b8 = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, b8, rem, rem2, ids_sorted + hb[8], ids8,
+                                              c8, 0, 32, st);
+    void* tmp8;
+    if ((rc = ws.get_raw("rg_tmp8", b8, &tmp8))) return rc;
+    HRPP_CK(cub::DeviceRadixSort::SortPairsDescending(tmp8, b8, rem, rem2, ids_sorted + hb[8],
+                                                      ids8, c8, 0, 32, st));
+    k_replay_block<CLOSEST, LIVE, STACK, kBlockReplay><<<c8, kBlockReplay, 0, st>>>(a, ids8, c8);
     HRPP_LAUNCHED();
   }
   return 0;
