@@ -226,14 +226,6 @@ int hrpp_set_live_rounds(int rounds);
 /* Key segments with at most `len` rays are replayed by one lane, longer ones
  * by a whole warp (default 32).  Affects speed only, never results. */
 int hrpp_set_consult_short(int len);
-/* Coherent traversal order (default 0): batches of >= 65536 rays are traced
- * in an order sorted by direction octant, quantized direction and origin
- * Morton code.  Permutes work only; results are identical.  Speed only. */
-int hrpp_set_trace_coherent(int on);
-/* Traversal kernel flavour: 0 (default) one ray per thread, 1 persistent
- * warps refilling finished lanes from per-warp ray chunks (faster on very
- * divergent waves, slower on coherent ones).  Speed only. */
-int hrpp_set_trace_persistent(int on);
 
 #ifdef __cplusplus
 }

@@ -50,12 +50,10 @@ def _load():
     L.hrpp_device_count.argtypes = [P]
     L.hrpp_set_live_rounds.argtypes = [C.c_int]
     L.hrpp_set_consult_short.argtypes = [C.c_int]
-    L.hrpp_set_trace_coherent.argtypes = [C.c_int]
     L.hrpp_gen_primary.argtypes = [P, P, C.c_double, C.c_double, I64, I64, I64, I64, I64,
                                    C.c_uint64, C.c_int, P, P, P]
     L.hrpp_spawn.argtypes = [P, P, P, P, P, P, I64, C.c_int, P, C.c_double, C.c_int, C.c_uint64,
                              P, P, P, P, P, P, P, P, P, P]
-    L.hrpp_set_trace_persistent.argtypes = [C.c_int]
     L.hrpp_profile_enable.argtypes = [C.c_int]
     L.hrpp_profile_read.argtypes = [P, P, C.c_int, C.c_int]
     L.hrpp_hash_rays.argtypes = [P, P, I64, C.c_int, P, P]
@@ -86,8 +84,7 @@ def _load():
                  "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
                  "hrpp_profile_enable", "hrpp_profile_read", "hrpp_table_set_deferred",
                  "hrpp_table_pending", "hrpp_set_consult_short",
-                 "hrpp_set_trace_persistent", "hrpp_gen_primary", "hrpp_spawn",
-                 "hrpp_set_trace_coherent", "hrpp_partition_by_owner"):
+                 "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner"):
         getattr(L, name).restype = C.c_int
     return L
 
@@ -114,8 +111,7 @@ EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device
             "hrpp_table_lookup", "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
             "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
             "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short",
-            "hrpp_set_trace_persistent", "hrpp_gen_primary", "hrpp_spawn",
-            "hrpp_set_trace_coherent", "hrpp_partition_by_owner")
+            "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner")
 
 PROFILE_STAGES = ("hash", "trace", "trace_queue", "group", "consult", "commit", "other")
 

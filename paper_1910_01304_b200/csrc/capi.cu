@@ -287,14 +287,6 @@ int hrpp_device_count(int* count) {
   HRPP_CK(cudaGetDeviceCount(count));
   return HRPP_OK;
 }
-int hrpp_set_trace_persistent(int on) {
-  g_trace_persistent = on != 0;
-  return HRPP_OK;
-}
-int hrpp_set_trace_coherent(int on) {
-  g_trace_coherent = on != 0;
-  return HRPP_OK;
-}
 int hrpp_set_consult_short(int len) {
   CHECK_ARG(len >= 0, "short segment length must be >= 0");
   g_consult_short = len;

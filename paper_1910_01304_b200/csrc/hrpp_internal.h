@@ -120,15 +120,12 @@ int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys
                 cudaStream_t st);
 int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err,
                        cudaStream_t st);
-// Traces n rays (or the device-counted queue ray_idx[0..*count_dev)).  With
-// g_trace_coherent, large batches are traced in a coherence order (direction
-// octant, quantized direction, origin Morton code) -- a permutation of the
-// work only; every ray's result is unchanged.
+// Traces n rays (or the device-counted queue ray_idx[0..*count_dev)), one
+// ray per thread.
 int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const double* tmin, const double* tmax, int32_t start, int64_t n,
                  const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
                  const int* err, cudaStream_t st, Workspace* ws = nullptr);
-extern int g_trace_coherent;
 
 // Group a batch of keys: stable sort (key, ray) and find key segments.
 struct Segments {
@@ -146,7 +143,6 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, 
 int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, int* count_dev,
                   cudaStream_t st);
 extern int g_consult_short;
-extern int g_trace_persistent;
 // values[i] for i < n with flags[i] != 0, in order, count to *count_dev
 int compact_by_flags(Workspace& ws, const int32_t* values, const uint8_t* flags, int64_t n,
                      int32_t* out, int* count_dev, cudaStream_t st);

@@ -23,11 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--res", default=None)
-    ap.add_argument("--persistent", type=int, default=0)
-    ap.add_argument("--coherent", type=int, default=0)
     a = ap.parse_args()
-    hb._lib.lib.hrpp_set_trace_persistent(a.persistent)
-    hb._lib.lib.hrpp_set_trace_coherent(a.coherent)
     res = tuple(int(x) for x in a.res.split("x")) if a.res else None
     sc = scenes.make_scene(a.config, resolution=res)
     b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
