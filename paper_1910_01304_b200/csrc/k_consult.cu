@@ -985,11 +985,22 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
   if ((rc = to_host(pin + 32, seg.nsegs, sizeof(int), st))) return rc;
+  // ray -> (segment, position) needs no table: queue it before waiting for
+  // the segment count, so the device stays busy across the host round trip
+  ConsultArgs a{};
+  Workspace& ws = t.ws;
+  if ((rc = ws.get("k_segofray", n, &a.seg_of_ray)) || (rc = ws.get("k_posofray", n, &a.pos_of_ray)))
+    return rc;
+  a.sidx = seg.sidx;
+  a.seg_id = seg.seg_id;
+  {
+    ProfScope ps(P_CONSULT, st);
+    k_seg_scatter<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
+    HRPP_LAUNCHED();
+  }
   HRPP_CK(cudaStreamSynchronize(st));
   int nsegs_h = *(volatile int*)(pin + 32);
   if ((rc = t.reserve(nsegs_h, n, st))) return rc;
-  Workspace& ws = t.ws;
-  ConsultArgs a{};
   a.nodes = b.nodes;
   a.tris = b.tris;
   a.depth = b.depth;
@@ -1014,8 +1025,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       (rc = ws.get("k_exlen", n, &a.seg_exlen)) || (rc = ws.get("k_napp", n, &a.seg_napp)) ||
       (rc = ws.get("k_cursor", n, &a.seg_cursor)) || (rc = ws.get("k_app", n, &a.app)) ||
       (rc = ws.get("k_appray", n, &a.app_ray)) || (rc = ws.get("k_state", n, &a.state)) ||
-      (rc = ws.get("k_f1", n, &a.seg_f1)) || (rc = ws.get("k_segofray", n, &a.seg_of_ray)) ||
-      (rc = ws.get("k_posofray", n, &a.pos_of_ray)))
+      (rc = ws.get("k_f1", n, &a.seg_f1)))
     return rc;
   const int grid = (int)((n + 127) / 128);
   LongList LL;
@@ -1026,8 +1036,6 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   {
     ProfScope ps(P_CONSULT, st);
     k_seg_lookup<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a, n);
-    HRPP_LAUNCHED();
-    k_seg_scatter<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
     HRPP_LAUNCHED();
   }
   const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;
