@@ -68,6 +68,9 @@ struct TraceOut {
   int64_t* vis = nullptr;
   uint8_t* known = nullptr;               // set to 1 for every traced ray
   unsigned long long* sums = nullptr;     // [0] += boxes, [1] += tris
+  int32_t* box32 = nullptr;               // per-ray counts, 32-bit (live mode)
+  int32_t* tri32 = nullptr;
+  bool zero_miss_t = false;               // t = 0 on a miss (live-mode outputs)
 };
 
 struct BvhDev {

@@ -85,6 +85,8 @@ struct ConsultArgs {
   const int32_t* f_leaf;
   const int64_t* f_box;
   const int64_t* f_tri;
+  const int32_t* f_box32;  // live: the fallback traversal's counts
+  const int32_t* f_tri32;
   const uint8_t* f_known;  // live only
   // outputs by ray index
   uint8_t* o_found;
@@ -230,14 +232,9 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
   else c.fp++;
   c.ob += acc.boxes;
   c.ot += acc.tris;
-  if (LIVE) {
-    const bool ff = a.f_found[idx];
-    c.bb += a.f_box[idx];
-    c.bt += a.f_tri[idx];
-    a.o_found[idx] = ff;
-    a.o_t[idx] = ff ? a.f_t[idx] : 0.0;
-    a.o_slot[idx] = ff ? a.f_slot[idx] : -1;
-    a.o_leaf[idx] = ff ? a.f_leaf[idx] : -1;
+  if (LIVE) {  // the outputs already hold the full traversal (written by it)
+    c.bb += a.f_box32[idx];
+    c.bt += a.f_tri32[idx];
   } else if (a.log_cls) {
     a.log_cls[idx] = neg ? 2 : 1;
     a.log_eval_box[idx] = acc.boxes;
@@ -1042,23 +1039,22 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   // suspend/resume rounds store states for every ray; the default path does not
   a.sparse_state = !(c.live && rounds > 0);
   if (c.live) {
-    uint8_t *f_found, *f_known;
-    double* f_t;
-    int32_t *f_slot, *f_leaf, *queue;
-    int64_t *f_box, *f_tri;
+    // The fallback traversal writes the wave's outputs directly (a ray that
+    // turns out a TP is overwritten by its entry result later; every other
+    // ray's output is its full traversal), and its counts as int32.
+    uint8_t* f_known;
+    int32_t *queue, *f_box, *f_tri;
     int* qcount;
-    if ((rc = ws.get("v_ffound", n, &f_found)) || (rc = ws.get("v_fknown", n, &f_known)) ||
-        (rc = ws.get("v_ft", n, &f_t)) || (rc = ws.get("v_fslot", n, &f_slot)) ||
-        (rc = ws.get("v_fleaf", n, &f_leaf)) || (rc = ws.get("v_fbox", n, &f_box)) ||
-        (rc = ws.get("v_ftri", n, &f_tri)) || (rc = ws.get("v_queue", n, &queue)) ||
+    if ((rc = ws.get("v_fknown", n, &f_known)) || (rc = ws.get("v_fbox32", n, &f_box)) ||
+        (rc = ws.get("v_ftri32", n, &f_tri)) || (rc = ws.get("v_queue", n, &queue)) ||
         (rc = ws.get("v_qcount", 1, &qcount)) || (rc = ws.get("v_need", n, &a.need)))
       return rc;
-    a.f_found = f_found;
-    a.f_t = f_t;
-    a.f_slot = f_slot;
-    a.f_leaf = f_leaf;
-    a.f_box = f_box;
-    a.f_tri = f_tri;
+    a.f_found = c.o_found;
+    a.f_t = c.o_t;
+    a.f_slot = c.o_slot;
+    a.f_leaf = c.o_leaf;
+    a.f_box32 = f_box;
+    a.f_tri32 = f_tri;
     a.f_known = f_known;
     a.o_found = c.o_found;
     a.o_t = c.o_t;
@@ -1073,13 +1069,14 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       HRPP_LAUNCHED();
     }
     TraceOut to;
-    to.found = f_found;
-    to.t = f_t;
-    to.slot = f_slot;
-    to.leaf = f_leaf;
-    to.box = f_box;
-    to.tri = f_tri;
+    to.found = c.o_found;
+    to.t = c.o_t;
+    to.slot = c.o_slot;
+    to.leaf = c.o_leaf;
+    to.box32 = f_box;
+    to.tri32 = f_tri;
     to.known = f_known;
+    to.zero_miss_t = true;  // hrpp/tracer.py:331-339: a live miss reports t = 0
     // rounds == 0: eval0 already marked every ray that is not a TP against the
     // wave-start entry; trace them, then one replay completes the wave.
     // rounds > 0: exact replay rounds, the last one speculative.

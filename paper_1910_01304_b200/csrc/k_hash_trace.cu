@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     Hit h = trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, a.start);
     const TraceOut& o = a.out;
     if (o.found) o.found[i] = h.found;
-    if (o.t) o.t[i] = h.t;
+    if (o.t) o.t[i] = (o.zero_miss_t && !h.found) ? 0.0 : h.t;
     if (o.slot) o.slot[i] = h.slot;
     if (o.leaf) o.leaf[i] = h.leaf;
     if (CLOSEST && (o.u || o.v)) {
@@ -166,6 +166,8 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     if (o.box) o.box[i] = h.boxes;
     if (o.tri) o.tri[i] = h.tris;
     if (o.vis) o.vis[i] = h.boxes;  // visited == box_tests (kernels.py:115-116)
+    if (o.box32) o.box32[i] = h.boxes;
+    if (o.tri32) o.tri32[i] = h.tris;
     if (o.known) o.known[i] = 1;
     sb = h.boxes;
     stt = h.tris;
