@@ -77,7 +77,6 @@ struct ConsultArgs {
   int32_t* app_ray;  // ray index that triggered each append (deferred mode)
   RayState* state;   // per ray index
   int32_t* seg_of_ray;  // per ray index: key segment
-  int32_t* pos_of_ray;  // per ray index: sorted position
   // full-traversal results by ray index (baseline in limit mode)
   const uint8_t* f_found;
   const double* f_t;
@@ -336,20 +335,24 @@ __global__ void k_seg_cursor(ConsultArgs a) {
       a.seg_cursor[s] = a.seg_start[s + 1];
       a.seg_napp[s] = 0;
     } else {
-      a.seg_cursor[s] = a.pos_of_ray[f1] + 1;
+      // sidx is ascending within a segment (stable sort): find f1's position
+      int32_t lo = a.seg_start[s], hi = a.seg_start[s + 1];
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (a.sidx[mid] < f1) lo = mid + 1;
+        else hi = mid;
+      }
+      a.seg_cursor[s] = lo + 1;
       a.seg_napp[s] = 1;
     }
   }
 }
 
-// Ray -> (segment, sorted position), scattered once per wave.
+// Ray -> segment, scattered once per wave.
 __global__ void k_seg_scatter(ConsultArgs a, int64_t n) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t i = a.sidx[p];
-    a.seg_of_ray[i] = a.seg_id[p] - 1;
-    a.pos_of_ray[i] = (int32_t)p;
-  }
+       p += (int64_t)gridDim.x * blockDim.x)
+    a.seg_of_ray[a.sidx[p]] = a.seg_id[p] - 1;
 }
 
 // Every ray against the entry as it stood at the start of the wave; ray
@@ -986,8 +989,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   // the segment count, so the device stays busy across the host round trip
   ConsultArgs a{};
   Workspace& ws = t.ws;
-  if ((rc = ws.get("k_segofray", n, &a.seg_of_ray)) || (rc = ws.get("k_posofray", n, &a.pos_of_ray)))
-    return rc;
+  if ((rc = ws.get("k_segofray", n, &a.seg_of_ray))) return rc;
   a.sidx = seg.sidx;
   a.seg_id = seg.seg_id;
   {
@@ -1124,7 +1126,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   }
   if (t.deferred)
     return table_collect_pending(t, seg, n, a.seg_napp, a.app, a.app_ray, err, st);
-  return table_commit(t, seg, n, a.seg_eid, a.seg_napp, a.app, err, st);
+  // one thread per key segment (nsegs_h of them), not per ray
+  return table_commit(t, seg, nsegs_h, a.seg_eid, a.seg_napp, a.app, err, st);
 }
 
 }  // namespace hrpp
