@@ -256,7 +256,8 @@ def run_ours(args, rank, world, local_rank):
             def trace_fn(Oo, Do, a, b):
                 return hb.trace_wave(bvh, table, mode, Oo, Do, a, b, closest, stats=stats)
             return key_sharded_wave(dist, trace_fn, lambda Oo, Do: hb.hash_rays(Oo, Do, cfg),
-                                    partition_by_owner, O, D, t0, t1, outputs=outputs)[0]
+                                    lambda k, w: partition_by_owner(k, w, device_counts=True),
+                                    O, D, t0, t1, outputs=outputs)[0]
         out, _ = hb.trace_wave(bvh, table, mode, O, D, t0, t1, closest, stats=stats,
                                outputs=outputs, defer_commit=multi and mode != "baseline")
         if multi and mode != "baseline":

@@ -182,7 +182,8 @@ int hrpp_table_pending(hrpp_table_t table, uint64_t *keys, int32_t *nodes, int32
 /* Exact multi-GPU mode (key sharding): owner of key k among
  * `world` ranks = (mix64(k) >> 32) % world.  perm (device int32[n]) receives
  * the local rays grouped by owner, ray order kept within each owner (stable);
- * counts (host int64[world]) the rays per owner.  After an all-to-all of the
+ * counts (int64[world], host or device) the rays per owner -- with a device
+ * array the call does not wait for the device.  After an all-to-all of the
  * permuted rays every owner holds all rays of its keys in global ray order
  * and its consult is the single-GPU consult restricted to those keys, so
  * hits, statistics and the union of the tables equal one GPU's at any world

@@ -37,6 +37,10 @@ __global__ void k_owner(const uint64_t* __restrict__ keys, int64_t n, uint32_t w
     if (hist[k]) atomicAdd(counts + k, (unsigned long long)hist[k]);
 }
 
+__global__ void k_counts_out(const unsigned long long* cnt, int world, long long* out) {
+  for (int k = threadIdx.x; k < world; k += blockDim.x) out[k] = (long long)cnt[k];
+}
+
 }  // namespace hrpp
 
 using namespace hrpp;
@@ -76,6 +80,15 @@ extern "C" int hrpp_partition_by_owner(const uint64_t* keys, int64_t n, int worl
                                               st));
     }
   }
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, counts) == cudaSuccess &&
+      (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)) {
+    // device counts: no host round trip (the caller exchanges them on the device)
+    k_counts_out<<<1, 256, 0, st>>>(cnt, world, (long long*)counts);
+    HRPP_LAUNCHED();
+    return HRPP_OK;
+  }
+  cudaGetLastError();  // a host pointer is not an error
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
   for (int k0 = 0; k0 < world; k0 += 32) {  // 32 counters per readback

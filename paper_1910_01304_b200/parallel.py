@@ -95,17 +95,22 @@ def merge_wave_records(table, dist, ray_offset: int = 0, group=None):
 # exact key sharding
 # ---------------------------------------------------------------------------
 
-def partition_by_owner(keys, world: int):
+def partition_by_owner(keys, world: int, device_counts: bool = False):
     """(perm, counts): this rank's rays grouped by key owner, ray order kept
     within each owner (hrpp_partition_by_owner).  ``keys`` is a CUDA uint64
-    tensor; perm is a CUDA int32 tensor, counts a host int64[world]."""
+    tensor; perm is a CUDA int32 tensor; counts a host int64[world], or with
+    ``device_counts`` a CUDA int64 tensor (no host round trip)."""
     if not (_lib.is_torch(keys) and keys.is_cuda):
         raise ValueError("partition_by_owner needs device keys (a CUDA tensor)")
     n = int(keys.shape[0])
     perm = _lib.empty(n, np.int32, like=keys)
-    counts = np.zeros(int(world), np.int64)
-    rc = _lib.lib.hrpp_partition_by_owner(_lib.ptr(keys), n, int(world), _lib.ptr(perm),
-                                          counts.ctypes.data_as(_lib.C.c_void_p),
+    if device_counts:
+        counts = _lib.empty(int(world), np.int64, like=keys) if world > 0 else None
+        cptr = _lib.ptr(counts)
+    else:
+        counts = np.zeros(max(int(world), 0), np.int64)
+        cptr = counts.ctypes.data_as(_lib.C.c_void_p)
+    rc = _lib.lib.hrpp_partition_by_owner(_lib.ptr(keys), n, int(world), _lib.ptr(perm), cptr,
                                           _lib.stream_of(keys))
     _lib.check(rc, "partition_by_owner")
     return perm, counts
@@ -145,11 +150,12 @@ def key_sharded_wave(dist, trace_fn, key_fn, partition_fn, O, D, tmins, tmaxs, o
     perm, counts = partition_fn(keys, world)
     perm = torch.as_tensor(perm, device=O.device).long()
     dev = O.device
-    send = torch.as_tensor(np.asarray(counts, np.int64), device=dev)
+    send = torch.as_tensor(counts, device=dev).to(torch.int64)
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
-    send_counts = [int(c) for c in np.asarray(counts)]
-    recv_counts = [int(c) for c in recv.cpu().tolist()]
+    both = torch.cat([send, recv]).cpu().tolist()  # the one host round trip
+    send_counts = [int(c) for c in both[:world]]
+    recv_counts = [int(c) for c in both[world:]]
     parts = [_a2a(dist, x.index_select(0, perm), send_counts, recv_counts, group)
              for x in (O, D, tmins, tmaxs)]
     hits, stats = trace_fn(*parts)

@@ -551,6 +551,10 @@ def test_partition_by_owner_matches_restatement(hb, world, oracle_mod):
         perm, counts = partition_by_owner(torch.from_numpy(keys).cuda(), world)
         rp, rc = oracle_mod.partition_by_owner_np(keys, world)
         assert np.array_equal(perm.cpu().numpy(), rp) and np.array_equal(counts, rc)
+        perm2, counts2 = partition_by_owner(torch.from_numpy(keys).cuda(), world,
+                                           device_counts=True)
+        assert counts2.is_cuda and np.array_equal(counts2.cpu().numpy(), rc)
+        assert np.array_equal(perm2.cpu().numpy(), rp)
     with pytest.raises(ValueError):
         partition_by_owner(torch.zeros(4, dtype=torch.uint64).cuda(), 0)
 
