@@ -71,6 +71,14 @@ struct TraceOut {
   int32_t* box32 = nullptr;               // per-ray counts, 32-bit (live mode)
   int32_t* tri32 = nullptr;
   bool zero_miss_t = false;               // t = 0 on a miss (live-mode outputs)
+  // live consult hook: a traced ray that hits a node not yet in its key's
+  // wave-start entry bids (atomicMin) to be its segment's first append
+  const int32_t* fa_seg_of_ray = nullptr;
+  const int64_t* fa_exoff = nullptr;
+  const int32_t* fa_exlen = nullptr;
+  const int32_t* fa_arena = nullptr;
+  const int32_t* fa_anc = nullptr;
+  int32_t* fa_f1 = nullptr;
 };
 
 struct BvhDev {

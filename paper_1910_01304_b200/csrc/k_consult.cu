@@ -950,10 +950,12 @@ static void dispatch_eval0(int stack, int grid, cudaStream_t st, const ConsultAr
 }
 
 static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
-                           const ConsultArgs& a, int64_t n) {
+                           const ConsultArgs& a, int64_t n, bool first_append_done = false) {
   ProfScope ps(P_CONSULT, st);
-  k_first_append<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
-  HRPP_LAUNCHED();
+  if (!first_append_done) {
+    k_first_append<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
+    HRPP_LAUNCHED();
+  }
   // about one resident wave of blocks: a thread walks several rays and each
   // block flushes its tallies once
   const int fgrid = grid_for(n, 128, num_sms() * 8);
@@ -1079,6 +1081,14 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     to.tri32 = f_tri;
     to.known = f_known;
     to.zero_miss_t = true;  // hrpp/tracer.py:331-339: a live miss reports t = 0
+    if (rounds == 0) {  // the queue is exactly k_first_append's candidate set
+      to.fa_seg_of_ray = a.seg_of_ray;
+      to.fa_exoff = a.seg_exoff;
+      to.fa_exlen = a.seg_exlen;
+      to.fa_arena = a.arena;
+      to.fa_anc = a.anc;
+      to.fa_f1 = a.seg_f1;
+    }
     // rounds == 0: eval0 already marked every ray that is not a TP against the
     // wave-start entry; trace them, then one replay completes the wave.
     // rounds > 0: exact replay rounds, the last one speculative.
@@ -1098,7 +1108,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     }
     a.spec = 0;
     if (rounds == 0) {
-      if ((rc = finalize_prefix(t.closest, true, grid, st, a, n))) return rc;
+      if ((rc = finalize_prefix(t.closest, true, grid, st, a, n, true))) return rc;
       if ((rc = launch_grouped(t.closest, true, b.stack, st, a, ws, nsegs_h))) return rc;
     } else {
       if ((rc = launch_replay(t.closest, true, b.stack, st, a, ws, LL, n))) return rc;

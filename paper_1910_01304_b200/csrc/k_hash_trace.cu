@@ -168,6 +168,15 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     if (o.vis) o.vis[i] = h.boxes;  // visited == box_tests (kernels.py:115-116)
     if (o.box32) o.box32[i] = h.boxes;
     if (o.tri32) o.tri32[i] = h.tris;
+    if (o.fa_f1 && h.found) {  // k_first_append's test, fused (k_consult.cu)
+      const int32_t s = o.fa_seg_of_ray[i];
+      const int32_t node = o.fa_anc[h.leaf];
+      const int64_t off = o.fa_exoff[s];
+      const int32_t len = o.fa_exlen[s];
+      bool dup = false;
+      for (int32_t k = 0; k < len && !dup; k++) dup = o.fa_arena[off + k] == node;
+      if (!dup) atomicMin(o.fa_f1 + s, (int32_t)i);
+    }
     if (o.known) o.known[i] = 1;
     sb = h.boxes;
     stt = h.tris;
