@@ -463,11 +463,13 @@ def test_deferred_commit_equals_direct_and_two_block_merge(hb):
 @pytest.mark.parametrize("short", [0, 1, 8, 100000])
 @pytest.mark.parametrize("mode", ["limit", "live"])
 def test_consult_paths_identical(hb, short, mode):
-    """Lane-per-segment and warp-per-segment replays give the same answers."""
+    """The suspend/resume replay (live rounds > 0): lane-per-segment and
+    warp-per-segment variants give the reference's answers."""
     inp = load_golden("wave_inputs.npz")
     ref = load_golden(f"wave_{mode}_p3_g0.npz")
     b = gbvh(hb, "spheres")
     hb.set_consult_short(short)
+    hb.set_live_rounds(2)
     try:
         t = hb.PredictorTable(hb.HashConfig(3), 0)
         stats = hb.RayKindStats()
@@ -480,6 +482,38 @@ def test_consult_paths_identical(hb, short, mode):
         assert list(t.dump_lines()) == list(ref["primary_dump"])
     finally:
         hb.set_consult_short(32)
+        hb.set_live_rounds(0)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("mode", ["limit", "live"])
+def test_very_long_key_segments_vs_oracle(hb, oracle_mod, p, mode):
+    """Coarse hashes put thousands of rays on one key (the block-per-segment
+    replay, > 1024 rays): GPU == C oracle on hits, stats and the table over a
+    primary wave and a bounce wave."""
+    from paper_1910_01304_b200 import scenes
+    sc = scenes.make_scene("c1")
+    b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
+    ob = oracle_mod.OracleBvh(b.bmin, b.bmax, b.left, b.right, b.axis, b.first, b.count,
+                              b.parent, b.depth, b.tv0, b.tv1, b.tv2, b.tri_ids)
+    O, D = scenes.primary_rays(sc.camera, sc.spp, seed=5)
+    n = O.shape[0]
+    keys = oracle_mod.hash_rays_np(O, D, p)
+    assert np.unique(keys, return_counts=True)[1].max() > 1024  # exercises the block path
+    base = hb.intersect_closest_batch(b, O, D, np.zeros(n), np.full(n, np.inf))
+    _, P, N = scenes.hit_frames(O, D, base["found"], base["t"], base["slot"],
+                                scenes.slot_normals(b.tv0, b.tv1, b.tv2))
+    waves = [(O, D, np.zeros(n), np.full(n, np.inf)), scenes.cosine_bounce(P, N, seed=2)]
+    t = hb.PredictorTable(hb.HashConfig(p), 0, hb.RayKind.CLOSEST_HIT)
+    ot = oracle_mod.OracleTable(p, 0, True)
+    for Ow, Dw, t0, t1 in waves:
+        out, st = hb.trace_wave(b, t, mode, Ow, Dw, t0, t1, True)
+        rc, ref, rst = oracle_mod.trace_wave(ob, ot, mode, True, Ow, Dw, t0, t1)
+        assert rc == 0
+        assert np.array_equal(st, rst), (st, rst)
+        for k in ("found", "t", "slot", "leaf"):
+            assert np.array_equal(out[k], ref[k]), k
+        assert list(t.dump_lines()) == ot.dump_lines()
 
 
 # -- ray generation and spawning on the device --------------------------------------------
