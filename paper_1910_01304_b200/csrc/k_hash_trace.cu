@@ -79,13 +79,152 @@ __global__ void __launch_bounds__(256) k_hash(const float* __restrict__ O,
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
 }
 
+// Bulk-copy (TMA) variant for large aligned batches: a persistent grid, each
+// block streaming 1024-ray tiles of O and D (2 x 12 KB) through a 4-stage
+// shared-memory ring filled by cp.async.bulk and signalled by mbarriers (one
+// elected thread issues; every thread hashes 4 rays of a landed tile), so
+// ~96 KB per block stay in flight while the previous tiles are hashed.
+constexpr int kHashTile = 1024;      // rays per tile (256 threads x 4)
+constexpr int kHashStages = 4;
+constexpr int kHashTileBytes = kHashTile * 12;  // one of O or D
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Arm the stage's barrier with the tile's byte count and start both copies
+// (bytes: a multiple of 48, i.e. whole groups of 4 rays; 0 for a tile of < 4).
+__device__ __forceinline__ void bulk_tile(uint32_t bar, uint32_t dst_o, uint32_t dst_d,
+                                          const float* src_o, const float* src_d,
+                                          uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(2 * bytes)
+               : "memory");
+  if (bytes == 0) return;
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst_o),
+      "l"(src_o), "r"(bytes), "r"(bar)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst_d),
+      "l"(src_d), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t tile_bytes(int64_t t, int64_t n) {
+  const int64_t rays = n - t * kHashTile < kHashTile ? n - t * kHashTile : kHashTile;
+  return (uint32_t)((rays / 4) * 48);
+}
+
+__global__ void __launch_bounds__(256) k_hash_bulk(const float* __restrict__ O,
+                                                   const float* __restrict__ D, int64_t n,
+                                                   int p, uint64_t* __restrict__ keys, int* err) {
+  const int64_t ntiles = (n + kHashTile - 1) / kHashTile;
+  extern __shared__ __align__(128) unsigned char hsm[];
+  float* so = reinterpret_cast<float*>(hsm);                                  // [stages][3072]
+  float* sd = reinterpret_cast<float*>(hsm + kHashStages * kHashTileBytes);  // [stages][3072]
+  __shared__ __align__(8) unsigned long long bars[kHashStages];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int sI = 0; sI < kHashStages; sI++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[sI])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // this block's tiles: blockIdx.x, + gridDim.x, ...
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t mine = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+  if (tid == 0)
+    for (int sI = 0; sI < kHashStages && sI < mine; sI++) {
+      const int64_t t = first + sI * stride;
+      bulk_tile(smem_u32(&bars[sI]), smem_u32(so + sI * (kHashTile * 3)),
+                smem_u32(sd + sI * (kHashTile * 3)), O + t * (kHashTile * 3),
+                D + t * (kHashTile * 3), tile_bytes(t, n));
+    }
+  bool bad = false;
+  for (int64_t k = 0; k < mine; k++) {
+    const int sI = (int)(k % kHashStages);
+    const uint32_t parity = (uint32_t)((k / kHashStages) & 1);
+    mbar_wait(smem_u32(&bars[sI]), parity);
+    const int64_t t = first + k * stride;
+    const int64_t i0 = t * kHashTile + 4 * tid;  // this thread's 4 rays
+    if (i0 + 4 > n) {  // the batch's last < 4 rays: straight from global
+      for (int64_t i = i0; i < n; i++) {
+        const uint32_t o0 = __float_as_uint(O[3 * i]), o1 = __float_as_uint(O[3 * i + 1]),
+                       o2 = __float_as_uint(O[3 * i + 2]);
+        const uint32_t d0 = __float_as_uint(D[3 * i]), d1 = __float_as_uint(D[3 * i + 1]),
+                       d2 = __float_as_uint(D[3 * i + 2]);
+        bad |= nonfinite(o0) | nonfinite(o1) | nonfinite(o2) | nonfinite(d0) | nonfinite(d1) |
+               nonfinite(d2);
+        keys[i] = ray_key(o0, o1, o2, d0, d1, d2, p);
+      }
+    } else {
+    const float4* o4 = reinterpret_cast<const float4*>(so + sI * (kHashTile * 3) + 12 * tid);
+    const float4* d4 = reinterpret_cast<const float4*>(sd + sI * (kHashTile * 3) + 12 * tid);
+    const float4 oa = o4[0], ob = o4[1], oc = o4[2];
+    const float4 da = d4[0], db = d4[1], dc = d4[2];
+    const uint32_t o[12] = {__float_as_uint(oa.x), __float_as_uint(oa.y), __float_as_uint(oa.z),
+                            __float_as_uint(oa.w), __float_as_uint(ob.x), __float_as_uint(ob.y),
+                            __float_as_uint(ob.z), __float_as_uint(ob.w), __float_as_uint(oc.x),
+                            __float_as_uint(oc.y), __float_as_uint(oc.z), __float_as_uint(oc.w)};
+    const uint32_t d[12] = {__float_as_uint(da.x), __float_as_uint(da.y), __float_as_uint(da.z),
+                            __float_as_uint(da.w), __float_as_uint(db.x), __float_as_uint(db.y),
+                            __float_as_uint(db.z), __float_as_uint(db.w), __float_as_uint(dc.x),
+                            __float_as_uint(dc.y), __float_as_uint(dc.z), __float_as_uint(dc.w)};
+#pragma unroll
+    for (int j = 0; j < 12; j++) bad |= nonfinite(o[j]) | nonfinite(d[j]);
+    ulonglong2 k01, k23;
+    k01.x = ray_key(o[0], o[1], o[2], d[0], d[1], d[2], p);
+    k01.y = ray_key(o[3], o[4], o[5], d[3], d[4], d[5], p);
+    k23.x = ray_key(o[6], o[7], o[8], d[6], d[7], d[8], p);
+    k23.y = ray_key(o[9], o[10], o[11], d[9], d[10], d[11], p);
+    ulonglong2* kp = reinterpret_cast<ulonglong2*>(keys + i0);
+    __stcs(kp, k01);
+    __stcs(kp + 1, k23);
+    }
+    __syncthreads();  // stage sI consumed by every thread: refill it
+    if (tid == 0 && k + kHashStages < mine) {
+      const int64_t tn = first + (k + kHashStages) * stride;
+      bulk_tile(smem_u32(&bars[sI]), smem_u32(so + sI * (kHashTile * 3)),
+                smem_u32(sd + sI * (kHashTile * 3)), O + tn * (kHashTile * 3),
+                D + tn * (kHashTile * 3), tile_bytes(tn, n));
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(err, 1);
+}
+
 int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys, int* err,
                 cudaStream_t st) {
   if (n <= 0) return 0;
-  int64_t nq = (n + 3) / 4;
-  int grid = grid_for(nq, 256, num_sms() * 8);
   ProfScope ps(P_HASH, st);
-  k_hash<<<grid, 256, 0, st>>>(O, D, n, p, keys, err);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(O) | reinterpret_cast<uintptr_t>(D) |
+                         reinterpret_cast<uintptr_t>(keys)) & 15) == 0;
+  const int64_t ntiles = (n + kHashTile - 1) / kHashTile;
+  if (aligned && ntiles >= 2 * (int64_t)num_sms()) {
+    static int smem_set = 0;
+    const int smem = 2 * kHashStages * kHashTileBytes;
+    if (!smem_set) {
+      HRPP_CK(cudaFuncSetAttribute(k_hash_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      smem_set = 1;
+    }
+    k_hash_bulk<<<2 * num_sms(), 256, smem, st>>>(O, D, n, p, keys, err);
+  } else {  // small or unaligned batches
+    k_hash<<<grid_for((n + 3) / 4, 256, num_sms() * 8), 256, 0, st>>>(O, D, n, p, keys, err);
+  }
   HRPP_LAUNCHED();
   return 0;
 }

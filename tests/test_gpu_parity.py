@@ -54,6 +54,25 @@ def test_hash_unaligned_and_ragged(hb):
             assert np.array_equal(keys, g["keys"][5][off:off + n])
 
 
+@pytest.mark.parametrize("n", [303104, 400003, 1 << 20])
+def test_hash_bulk_copy_path(hb, oracle_mod, n):
+    """Large aligned batches take the TMA bulk-copy kernel (1024-ray tiles,
+    a partial last tile, < 4 trailing rays): keys == numpy restatement, and a
+    non-finite component anywhere is still reported."""
+    import torch
+    rng = np.random.default_rng(n)
+    O = rng.normal(size=(n, 3)).astype(np.float32) * 7
+    D = rng.normal(size=(n, 3)).astype(np.float32)
+    cfg = hb.HashConfig(6)
+    keys = hb.hash_rays(torch.from_numpy(O).cuda(), torch.from_numpy(D).cuda(), cfg)
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), oracle_mod.hash_rays_np(O, D, 6))
+    for bad_at in (0, n // 2, n - 1):
+        Ob = O.copy()
+        Ob[bad_at, 1] = np.inf
+        with pytest.raises(hb.NonFiniteInput):
+            hb.hash_rays(torch.from_numpy(Ob).cuda(), torch.from_numpy(D).cuda(), cfg)
+
+
 def test_hash_known_answers_and_scalars(hb):
     cfg2 = hb.HashConfig(2)
     assert hb.map_float_to_hash(1.0, cfg2) == 4
