@@ -593,17 +593,20 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
   int32_t applied = 0;
   if (valid) get_state<CLOSEST>(a, idx, ex_len, acc, applied);
   int32_t L = ex_len + napp;
-  int32_t cnode = -1;
-  // a TP's full result may never have been computed (live): read only known ones
-  if (valid && (!LIVE || a.f_known[idx]) && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
-  bool inL = false;
-  if (valid)
-    for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
   Ray r{};
   if (valid) {
     r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
     if (applied < L && (CLOSEST || !acc.found))
       catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+  }
+  // The record node (anc of the full-traversal leaf) matters only to a ray
+  // that is not a TP now -- a TP stays one -- so only those lanes read it
+  // (a TP's full result may never have been computed in live mode anyway).
+  int32_t cnode = -1;
+  bool inL = false;
+  if (valid && (L == 0 || !acc.found) && (!LIVE || a.f_known[idx]) && a.f_found[idx]) {
+    cnode = a.anc[a.f_leaf[idx]];
+    for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
   }
   // Step from append to append: the rays before the next ray that grows the
   // entry see a constant list, so they are classified together (TP, or
@@ -681,16 +684,17 @@ __global__ void __launch_bounds__(BS, BS == 32 ? 16 : HRPP_BLOCK_MINB)
       int32_t applied = 0;
       if (valid) get_state<CLOSEST>(a, idx, ex_len, acc, applied);
       int32_t L = ex_len + napp;
-      int32_t cnode = -1;
-      if (valid && (!LIVE || a.f_known[idx]) && a.f_found[idx]) cnode = a.anc[a.f_leaf[idx]];
-      bool inL = false;
-      if (cnode >= 0)
-        for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
       Ray r{};
       if (valid) {
         r = make_ray(a.O, a.D, a.tmin, a.tmax, idx);
         if (applied < L && (CLOSEST || !acc.found))
           catch_up<CLOSEST, STACK>(a, r, acc, applied, L, ex_off, ex_len, app);
+      }
+      int32_t cnode = -1;  // read only by rays that are not TPs now (see k_replay_group)
+      bool inL = false;
+      if (valid && (L == 0 || !acc.found) && (!LIVE || a.f_known[idx]) && a.f_found[idx]) {
+        cnode = a.anc[a.f_leaf[idx]];
+        for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
       }
       // append to append, as in k_replay_group
       int cursor = 0;
