@@ -348,28 +348,26 @@ __global__ void k_seg_cursor(ConsultArgs a) {
   }
 }
 
-// Ray -> segment, scattered once per wave.
-__global__ void k_seg_scatter(ConsultArgs a, int64_t n) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x)
-    a.seg_of_ray[a.sidx[p]] = a.seg_id[p] - 1;
-}
 
-// Every ray against the entry as it stood at the start of the wave; ray
-// order, so ray, state and flag accesses are coalesced.
+// Every ray against the entry as it stood at the start of the wave, fused
+// with the ray -> segment scatter: threads walk sorted positions (segment
+// data coalesced, one random 4-B store per ray); only rays whose key already
+// had an entry read their ray and evaluate it.
 template <bool CLOSEST, int STACK>
 __global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
   if (*a.err) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = a.seg_of_ray[i];
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = a.sidx[p];
+    const int32_t s = a.seg_id[p] - 1;
+    a.seg_of_ray[i] = s;
     const int32_t ex_len = a.seg_exlen[s];
     Hit acc = empty_entry_result(CLOSEST);
     if (ex_len > 0) {
       const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
       catch_up<CLOSEST, STACK>(a, r, acc, 0, ex_len, a.seg_exoff[s], ex_len, nullptr);
     }
-    if (ex_len > 0 || !a.sparse_state) store_state(a, (int32_t)i, acc, ex_len);
+    if (ex_len > 0 || !a.sparse_state) store_state(a, i, acc, ex_len);
     if (mark_need) a.need[i] = !(ex_len > 0 && acc.found);
   }
 }
@@ -991,18 +989,9 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
   if ((rc = to_host(pin + 32, seg.nsegs, sizeof(int), st))) return rc;
-  // ray -> (segment, position) needs no table: queue it before waiting for
-  // the segment count, so the device stays busy across the host round trip
   ConsultArgs a{};
   Workspace& ws = t.ws;
   if ((rc = ws.get("k_segofray", n, &a.seg_of_ray))) return rc;
-  a.sidx = seg.sidx;
-  a.seg_id = seg.seg_id;
-  {
-    ProfScope ps(P_CONSULT, st);
-    k_seg_scatter<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
-    HRPP_LAUNCHED();
-  }
   HRPP_CK(cudaStreamSynchronize(st));
   int nsegs_h = *(volatile int*)(pin + 32);
   if ((rc = t.reserve(nsegs_h, n, st))) return rc;
@@ -1069,7 +1058,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.o_slot = c.o_slot;
     a.o_leaf = c.o_leaf;
     HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
-    HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
+    if (rounds > 0) HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));  // else eval0 writes all
     {
       ProfScope ps(P_CONSULT, st);
       if (t.closest) dispatch_eval0<true>(b.stack, grid, st, a, n, rounds == 0);
