@@ -325,28 +325,6 @@ __global__ void __launch_bounds__(128, HRPP_FIN_MINB) k_finalize(ConsultArgs a, 
   flush_tally(c, a.stats);
 }
 
-// Replay cursor per segment: right after its first append, or done.
-__global__ void k_seg_cursor(ConsultArgs a) {
-  const int ns = *a.nsegs;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t f1 = a.seg_f1[s];
-    if (f1 == 0x7fffffff) {
-      a.seg_cursor[s] = a.seg_start[s + 1];
-      a.seg_napp[s] = 0;
-    } else {
-      // sidx is ascending within a segment (stable sort): find f1's position
-      int32_t lo = a.seg_start[s], hi = a.seg_start[s + 1];
-      while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        if (a.sidx[mid] < f1) lo = mid + 1;
-        else hi = mid;
-      }
-      a.seg_cursor[s] = lo + 1;
-      a.seg_napp[s] = 1;
-    }
-  }
-}
 
 
 // Every ray against the entry as it stood at the start of the wave, fused
@@ -750,13 +728,28 @@ __global__ void k_seg_remaining(ConsultArgs a, const int32_t* list, int m, int32
 
 // Replay length class of every segment (rays left): 0 done, 1..6 for
 // <= 1, 2, 4, 8, 16, 32 rays, 7 up to kBlockReplayMin, 8 longer.
+// (Also sets each segment's replay cursor: right after its first append, or
+// done -- k_seg_cursor's job, fused.)
 __global__ void k_replay_class(ConsultArgs a, int64_t nseg_cap, uint8_t* cls, int32_t* ids) {
   const int ns = *a.nsegs;
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg_cap;
        s += (int64_t)gridDim.x * blockDim.x) {
     int k = 0;
     if (s < ns) {
-      const int32_t rem = a.seg_start[s + 1] - a.seg_cursor[s];
+      const int32_t f1 = a.seg_f1[s], end = a.seg_start[s + 1];
+      int32_t cur = end;
+      if (f1 != 0x7fffffff) {  // sidx ascends within a segment: f1's position
+        int32_t lo = a.seg_start[s], hi = end;
+        while (lo < hi) {
+          const int32_t mid = (lo + hi) >> 1;
+          if (a.sidx[mid] < f1) lo = mid + 1;
+          else hi = mid;
+        }
+        cur = lo + 1;
+      }
+      a.seg_cursor[s] = cur;
+      a.seg_napp[s] = f1 != 0x7fffffff ? 1 : 0;
+      const int32_t rem = end - cur;
       k = rem <= 0 ? 0 : rem <= 1 ? 1 : rem <= 2 ? 2 : rem <= 4 ? 3 : rem <= 8 ? 4
         : rem <= 16 ? 5 : rem <= 32 ? 6 : rem <= kBlockReplayMin ? 7 : 8;
     }
@@ -970,9 +963,7 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
     else k_finalize<false, false><<<fgrid, 128, 0, st>>>(a, n);
   }
   HRPP_LAUNCHED();
-  k_seg_cursor<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a);
-  HRPP_LAUNCHED();
-  return 0;
+  return 0;  // the replay cursors are set by k_replay_class
 }
 
 int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* keys,
