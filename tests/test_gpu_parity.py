@@ -650,3 +650,35 @@ def test_key_sharding_invariant_one_gpu(hb, mode):
     for c in (True, False):
         assert sorted(sum((list(t[c].dump_lines()) for t in own), [])) == \
             list(full[c].dump_lines())
+
+
+@pytest.mark.parametrize("mode", ["limit", "live"])
+def test_c2_full_frame_vs_oracle(hb, oracle_mod, mode):
+    """The headline workload at full size (BASELINE c2: 60k triangles,
+    1024x1024 spp 8, primary + area-light shadow + diffuse bounce, 18.7 M
+    rays): every hit, every statistic and both tables equal the C oracle's
+    sequential consult (its traversal batch uses all host threads)."""
+    import sys
+    from argparse import Namespace
+    from conftest import ROOT
+    sys.path.insert(0, str(ROOT))
+    import bench
+    args = Namespace(config="c2", res=None, spp=None, precision=6, go_up=0)
+    sc, b, waves = bench.make_workload(args, lambda bv, O, D, t0, t1:
+                                       hb.intersect_closest_batch(bv, O, D, t0, t1))
+    ob = oracle_mod.OracleBvh(b.bmin, b.bmax, b.left, b.right, b.axis, b.first, b.count,
+                              b.parent, b.depth, b.tv0, b.tv1, b.tv2, b.tri_ids)
+    cfg = hb.HashConfig(6)
+    tabs = {c: hb.PredictorTable(cfg, 0, hb.RayKind.CLOSEST_HIT if c else hb.RayKind.HIT_ANY)
+            for c in (True, False)}
+    otabs = {c: oracle_mod.OracleTable(6, 0, c) for c in (True, False)}
+    for name, kind, closest, O, D, t0, t1 in waves:
+        out, st = hb.trace_wave(b, tabs[closest], mode, O, D, t0, t1, closest)
+        rc, ref, rst = oracle_mod.trace_wave(ob, otabs[closest], mode, closest, O, D, t0, t1)
+        assert rc == 0
+        assert np.array_equal(st, rst), (name, st, rst)
+        for k in ("found", "t", "slot", "leaf"):
+            assert np.array_equal(out[k], ref[k]), (name, k)
+    for c in (True, False):
+        for g, r in zip(tabs[c].export(), otabs[c].export()):
+            assert np.array_equal(g, r)
