@@ -219,6 +219,9 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t table, int mode, int closest,
  * 6 other.  hrpp_profile_read synchronizes the device and returns the
  * accumulated milliseconds and stage counts (number of stages = 7). */
 int hrpp_profile_enable(int on);
+/* Record only the stages whose bit is set in `mask` (bit = stage index);
+ * 0 disables.  Fewer events keep the profiler out of the timed path. */
+int hrpp_profile_stages(unsigned mask);
 int hrpp_profile_read(double *ms, int64_t *counts, int n, int reset);
 
 /* Live-mode speculation policy (rounds of exact per-key scan before the

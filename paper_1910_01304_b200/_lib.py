@@ -55,6 +55,7 @@ def _load():
     L.hrpp_spawn.argtypes = [P, P, P, P, P, P, I64, C.c_int, P, C.c_double, C.c_int, C.c_uint64,
                              P, P, P, P, P, P, P, P, P, P]
     L.hrpp_profile_enable.argtypes = [C.c_int]
+    L.hrpp_profile_stages.argtypes = [C.c_uint]
     L.hrpp_profile_read.argtypes = [P, P, C.c_int, C.c_int]
     L.hrpp_hash_rays.argtypes = [P, P, I64, C.c_int, P, P]
     L.hrpp_hash_floats.argtypes = [P, I64, C.c_int, P, P]
@@ -84,7 +85,8 @@ def _load():
                  "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
                  "hrpp_profile_enable", "hrpp_profile_read", "hrpp_table_set_deferred",
                  "hrpp_table_pending", "hrpp_set_consult_short",
-                 "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner"):
+                 "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner",
+                 "hrpp_profile_stages"):
         getattr(L, name).restype = C.c_int
     return L
 
@@ -111,13 +113,22 @@ EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device
             "hrpp_table_lookup", "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
             "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
             "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short",
-            "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner")
+            "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner",
+            "hrpp_profile_stages")
 
 PROFILE_STAGES = ("hash", "trace", "trace_queue", "group", "consult", "commit", "other")
 
 
-def profile_enable(on: bool = True):
-    lib.hrpp_profile_enable(int(bool(on)))
+def profile_enable(on: bool = True, stages=None):
+    """Enable the per-stage event profiler (all stages, or only the named
+    ones: fewer events disturb the timed path less)."""
+    if stages is None:
+        lib.hrpp_profile_enable(int(bool(on)))
+    else:
+        mask = 0
+        for k in stages:
+            mask |= 1 << PROFILE_STAGES.index(k)
+        lib.hrpp_profile_stages(mask if on else 0)
 
 
 def profile_read(reset: bool = True) -> dict:

@@ -99,6 +99,7 @@ int BvhDev::ancestor_lut(int level, const int32_t** out) {
 // Calls may run concurrently from several host threads (one stream each, e.g.
 // waves on different tables); the profiler's shared state is under a mutex.
 bool g_prof_on = false;
+static unsigned g_prof_mask = ~0u;  // stages recorded while enabled
 static std::mutex g_prof_mu;
 struct ProfState {
   std::vector<cudaEvent_t> pool;
@@ -119,7 +120,7 @@ struct ProfState {
 static ProfState g_prof;
 
 ProfScope::ProfScope(int c, cudaStream_t s) : cat(c), st(s) {
-  if (!g_prof_on) return;
+  if (!g_prof_on || !((g_prof_mask >> c) & 1u)) return;
   {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     a = g_prof.get();
@@ -294,6 +295,12 @@ int hrpp_set_consult_short(int len) {
 }
 int hrpp_profile_enable(int on) {
   g_prof_on = on != 0;
+  g_prof_mask = ~0u;
+  return HRPP_OK;
+}
+int hrpp_profile_stages(unsigned mask) {
+  g_prof_on = mask != 0;
+  g_prof_mask = mask;
   return HRPP_OK;
 }
 int hrpp_profile_read(double* ms, int64_t* counts, int n, int reset) {
