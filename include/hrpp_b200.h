@@ -190,6 +190,18 @@ int hrpp_table_pending(hrpp_table_t table, uint64_t *keys, int32_t *nodes, int32
  * size.  keys: device uint64[n] from hrpp_hash_rays. */
 int hrpp_partition_by_owner(const uint64_t *keys, int64_t n, int world, int32_t *perm,
                             int64_t *counts, void *stream);
+/* Key-sharding exchange rows (device arrays; one all-to-all each way):
+ * a ray row is 40 B {O.xyz f32, D.xyz f32, tmin f64, tmax f64}, gathered in
+ * `perm` order; a hit row is 24 B {t f64, slot i32, leaf i32, found u8, pad},
+ * scattered back to positions perm[k]. */
+int hrpp_pack_rays(const int32_t *perm, int64_t n, const float *O, const float *D,
+                   const double *tmin, const double *tmax, void *rows, void *stream);
+int hrpp_unpack_rays(const void *rows, int64_t n, float *O, float *D, double *tmin,
+                     double *tmax, void *stream);
+int hrpp_pack_hits(int64_t n, const uint8_t *found, const double *t, const int32_t *slot,
+                   const int32_t *leaf, void *rows, void *stream);
+int hrpp_unpack_hits(const void *rows, const int32_t *perm, int64_t n, uint8_t *found,
+                     double *t, int32_t *slot, int32_t *leaf, void *stream);
 
 /* ---- predict: hrpp/predictor.py:167-192 over a batch, frozen table ------ */
 /* cls 0 TP / 1 FP / 2 NEG; t/slot/leaf/u/v of the entry result (t = inf for

@@ -74,6 +74,10 @@ def _load():
     L.hrpp_table_set_deferred.argtypes = [P, C.c_int]
     L.hrpp_table_pending.argtypes = [P, P, P, P, I64, P]
     L.hrpp_partition_by_owner.argtypes = [P, I64, C.c_int, P, P, P]
+    L.hrpp_pack_rays.argtypes = [P, I64, P, P, P, P, P, P]
+    L.hrpp_unpack_rays.argtypes = [P, I64, P, P, P, P, P]
+    L.hrpp_pack_hits.argtypes = [I64, P, P, P, P, P, P]
+    L.hrpp_unpack_hits.argtypes = [P, P, I64, P, P, P, P, P]
     L.hrpp_predict_batch.argtypes = [P, P, P, P, P, P, P, I64] + [P] * 10 + [P]
     L.hrpp_trace_wave.argtypes = [P, P, C.c_int, C.c_int, P, P, P, P, I64, C.POINTER(WaveOut),
                                   C.POINTER(OutcomeLogC), P, P]
@@ -86,7 +90,8 @@ def _load():
                  "hrpp_profile_enable", "hrpp_profile_read", "hrpp_table_set_deferred",
                  "hrpp_table_pending", "hrpp_set_consult_short",
                  "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner",
-                 "hrpp_profile_stages"):
+                 "hrpp_profile_stages", "hrpp_pack_rays", "hrpp_unpack_rays",
+                 "hrpp_pack_hits", "hrpp_unpack_hits"):
         getattr(L, name).restype = C.c_int
     return L
 
@@ -114,7 +119,8 @@ EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device
             "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
             "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short",
             "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner",
-            "hrpp_profile_stages")
+            "hrpp_profile_stages", "hrpp_pack_rays", "hrpp_unpack_rays", "hrpp_pack_hits",
+            "hrpp_unpack_hits")
 
 PROFILE_STAGES = ("hash", "trace", "trace_queue", "group", "consult", "commit", "other")
 

@@ -37,6 +37,77 @@ __global__ void k_owner(const uint64_t* __restrict__ keys, int64_t n, uint32_t w
     if (hist[k]) atomicAdd(counts + k, (unsigned long long)hist[k]);
 }
 
+// Exchange rows (one all-to-all each way instead of four): a ray is 40 bytes
+// {O.xyz f32, D.xyz f32, tmin f64, tmax f64}; a hit is 24 bytes {t f64,
+// slot i32, leaf i32, found u8, pad}.
+struct __align__(8) RayRow {
+  float o[3], d[3];
+  double t0, t1;
+};
+struct __align__(8) HitRow {
+  double t;
+  int32_t slot, leaf;
+  uint8_t found;
+  uint8_t pad[7];
+};
+
+__global__ void k_pack_rays(const int32_t* __restrict__ perm, int64_t n,
+                            const float* __restrict__ O, const float* __restrict__ D,
+                            const double* __restrict__ t0, const double* __restrict__ t1,
+                            RayRow* __restrict__ rows) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = perm[k];
+    RayRow r;
+    r.o[0] = O[3 * i]; r.o[1] = O[3 * i + 1]; r.o[2] = O[3 * i + 2];
+    r.d[0] = D[3 * i]; r.d[1] = D[3 * i + 1]; r.d[2] = D[3 * i + 2];
+    r.t0 = t0[i];
+    r.t1 = t1[i];
+    rows[k] = r;
+  }
+}
+
+__global__ void k_unpack_rays(const RayRow* __restrict__ rows, int64_t n, float* __restrict__ O,
+                              float* __restrict__ D, double* __restrict__ t0,
+                              double* __restrict__ t1) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const RayRow r = rows[k];
+    O[3 * k] = r.o[0]; O[3 * k + 1] = r.o[1]; O[3 * k + 2] = r.o[2];
+    D[3 * k] = r.d[0]; D[3 * k + 1] = r.d[1]; D[3 * k + 2] = r.d[2];
+    t0[k] = r.t0;
+    t1[k] = r.t1;
+  }
+}
+
+__global__ void k_pack_hits(int64_t n, const uint8_t* __restrict__ found,
+                            const double* __restrict__ t, const int32_t* __restrict__ slot,
+                            const int32_t* __restrict__ leaf, HitRow* __restrict__ rows) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    HitRow h{};
+    h.t = t[k];
+    h.slot = slot[k];
+    h.leaf = leaf[k];
+    h.found = found[k];
+    rows[k] = h;
+  }
+}
+
+__global__ void k_unpack_hits(const HitRow* __restrict__ rows, const int32_t* __restrict__ perm,
+                              int64_t n, uint8_t* __restrict__ found, double* __restrict__ t,
+                              int32_t* __restrict__ slot, int32_t* __restrict__ leaf) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const HitRow h = rows[k];
+    const int64_t i = perm[k];
+    found[i] = h.found;
+    t[i] = h.t;
+    slot[i] = h.slot;
+    leaf[i] = h.leaf;
+  }
+}
+
 __global__ void k_counts_out(const unsigned long long* cnt, int world, long long* out) {
   for (int k = threadIdx.x; k < world; k += blockDim.x) out[k] = (long long)cnt[k];
 }
@@ -97,5 +168,59 @@ extern "C" int hrpp_partition_by_owner(const uint64_t* keys, int64_t n, int worl
     HRPP_CK(cudaStreamSynchronize(st));
     for (int k = 0; k < m2; k++) counts[k0 + k] = ((volatile long long*)pin)[32 + k];
   }
+  return HRPP_OK;
+}
+
+extern "C" int hrpp_pack_rays(const int32_t* perm, int64_t n, const float* O, const float* D,
+                              const double* tmin, const double* tmax, void* rows, void* stream) {
+  if (n < 0 || (n > 0 && (!perm || !O || !D || !tmin || !tmax || !rows))) {
+    set_error("pack_rays: bad arguments");
+    return HRPP_INVALID_ARG;
+  }
+  if (n == 0) return HRPP_OK;
+  k_pack_rays<<<grid_for(n, 256, num_sms() * 16), 256, 0, (cudaStream_t)stream>>>(
+      perm, n, O, D, tmin, tmax, (RayRow*)rows);
+  HRPP_LAUNCHED();
+  return HRPP_OK;
+}
+
+extern "C" int hrpp_unpack_rays(const void* rows, int64_t n, float* O, float* D, double* tmin,
+                                double* tmax, void* stream) {
+  if (n < 0 || (n > 0 && (!rows || !O || !D || !tmin || !tmax))) {
+    set_error("unpack_rays: bad arguments");
+    return HRPP_INVALID_ARG;
+  }
+  if (n == 0) return HRPP_OK;
+  k_unpack_rays<<<grid_for(n, 256, num_sms() * 16), 256, 0, (cudaStream_t)stream>>>(
+      (const RayRow*)rows, n, O, D, tmin, tmax);
+  HRPP_LAUNCHED();
+  return HRPP_OK;
+}
+
+extern "C" int hrpp_pack_hits(int64_t n, const uint8_t* found, const double* t,
+                              const int32_t* slot, const int32_t* leaf, void* rows,
+                              void* stream) {
+  if (n < 0 || (n > 0 && (!found || !t || !slot || !leaf || !rows))) {
+    set_error("pack_hits: bad arguments");
+    return HRPP_INVALID_ARG;
+  }
+  if (n == 0) return HRPP_OK;
+  k_pack_hits<<<grid_for(n, 256, num_sms() * 16), 256, 0, (cudaStream_t)stream>>>(
+      n, found, t, slot, leaf, (HitRow*)rows);
+  HRPP_LAUNCHED();
+  return HRPP_OK;
+}
+
+extern "C" int hrpp_unpack_hits(const void* rows, const int32_t* perm, int64_t n,
+                                uint8_t* found, double* t, int32_t* slot, int32_t* leaf,
+                                void* stream) {
+  if (n < 0 || (n > 0 && (!rows || !perm || !found || !t || !slot || !leaf))) {
+    set_error("unpack_hits: bad arguments");
+    return HRPP_INVALID_ARG;
+  }
+  if (n == 0) return HRPP_OK;
+  k_unpack_hits<<<grid_for(n, 256, num_sms() * 16), 256, 0, (cudaStream_t)stream>>>(
+      (const HitRow*)rows, perm, n, found, t, slot, leaf);
+  HRPP_LAUNCHED();
   return HRPP_OK;
 }

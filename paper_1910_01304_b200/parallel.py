@@ -148,7 +148,8 @@ def key_sharded_wave(dist, trace_fn, key_fn, partition_fn, O, D, tmins, tmaxs, o
     world = dist.get_world_size(group)
     keys = key_fn(O, D)
     perm, counts = partition_fn(keys, world)
-    perm = torch.as_tensor(perm, device=O.device).long()
+    perm32 = torch.as_tensor(perm, device=O.device).to(torch.int32).contiguous()
+    perm = perm32.long()
     dev = O.device
     send = torch.as_tensor(counts, device=dev).to(torch.int64)
     recv = torch.empty_like(send)
@@ -156,14 +157,69 @@ def key_sharded_wave(dist, trace_fn, key_fn, partition_fn, O, D, tmins, tmaxs, o
     both = torch.cat([send, recv]).cpu().tolist()  # the one host round trip
     send_counts = [int(c) for c in both[:world]]
     recv_counts = [int(c) for c in both[world:]]
+    n = int(O.shape[0])
+    out = dict(outputs) if outputs else {}
+    if dev.type == "cuda":  # one all-to-all each way, rows packed on the device
+        parts = _exchange_rays(dist, perm32, O, D, tmins, tmaxs, send_counts, recv_counts,
+                               group)
+        hits, stats = trace_fn(*parts)
+        _exchange_hits(dist, hits, perm32, n, out, recv_counts, send_counts, group)
+        return out, stats
+    # host tensors (the gloo tests): the same exchange, one field at a time
     parts = [_a2a(dist, x.index_select(0, perm), send_counts, recv_counts, group)
              for x in (O, D, tmins, tmaxs)]
     hits, stats = trace_fn(*parts)
-    n = int(O.shape[0])
-    out = dict(outputs) if outputs else {}
     for k in HIT_FIELDS:
         back = _a2a(dist, torch.as_tensor(hits[k], device=dev), recv_counts, send_counts, group)
         if k not in out:
             out[k] = torch.empty(n, dtype=back.dtype, device=dev)
         out[k].index_copy_(0, perm, back.to(out[k].dtype))
     return out, stats
+
+
+def _exchange_rays(dist, perm32, O, D, tmins, tmaxs, send_counts, recv_counts, group):
+    """Gather this rank's rays in owner order into 40-byte rows
+    (hrpp_pack_rays), all-to-all them, unpack the received rows."""
+    import torch
+    dev = O.device
+    st = _lib.stream_of(O)
+    n = int(O.shape[0])
+    O = O.reshape(-1, 3).to(torch.float32).contiguous()
+    D = D.reshape(-1, 3).to(torch.float32).contiguous()
+    t0 = tmins.reshape(-1).to(torch.float64).contiguous()
+    t1 = tmaxs.reshape(-1).to(torch.float64).contiguous()
+    rows = torch.empty((n, 40), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib.hrpp_pack_rays(_lib.ptr(perm32), n, _lib.ptr(O), _lib.ptr(D),
+                                       _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(rows), st),
+               "pack_rays")
+    got = _a2a(dist, rows, send_counts, recv_counts, group)
+    m = int(got.shape[0])
+    Or = torch.empty((m, 3), dtype=torch.float32, device=dev)
+    Dr = torch.empty((m, 3), dtype=torch.float32, device=dev)
+    t0r = torch.empty(m, dtype=torch.float64, device=dev)
+    t1r = torch.empty(m, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib.hrpp_unpack_rays(_lib.ptr(got), m, _lib.ptr(Or), _lib.ptr(Dr),
+                                         _lib.ptr(t0r), _lib.ptr(t1r), st), "unpack_rays")
+    return Or, Dr, t0r, t1r
+
+
+def _exchange_hits(dist, hits, perm32, n, out, send_counts, recv_counts, group):
+    """Pack the owner's hits into 24-byte rows (hrpp_pack_hits), send them
+    back, and scatter them to this rank's ray order (hrpp_unpack_hits)."""
+    import torch
+    f = hits["found"]
+    dev = f.device
+    st = _lib.stream_of(f)
+    m = int(f.shape[0])
+    cols = [torch.as_tensor(hits[k], device=dev).to(dt).contiguous()
+            for k, dt in zip(HIT_FIELDS, (torch.bool, torch.float64, torch.int32, torch.int32))]
+    rows = torch.empty((m, 24), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib.hrpp_pack_hits(m, *(_lib.ptr(c) for c in cols), _lib.ptr(rows), st),
+               "pack_hits")
+    back = _a2a(dist, rows, send_counts, recv_counts, group)
+    for k, dt in zip(HIT_FIELDS, (torch.bool, torch.float64, torch.int32, torch.int32)):
+        if k not in out or out[k].dtype != dt or not out[k].is_contiguous():
+            out[k] = torch.empty(n, dtype=dt, device=dev)
+    _lib.check(_lib.lib.hrpp_unpack_hits(_lib.ptr(back), _lib.ptr(perm32), n,
+                                         *(_lib.ptr(out[k]) for k in HIT_FIELDS), st),
+               "unpack_hits")

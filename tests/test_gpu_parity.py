@@ -682,3 +682,37 @@ def test_c2_full_frame_vs_oracle(hb, oracle_mod, mode):
     for c in (True, False):
         for g, r in zip(tabs[c].export(), otabs[c].export()):
             assert np.array_equal(g, r)
+
+
+def test_exchange_rows_round_trip(hb):
+    """The key-sharding exchange rows: packing rays in owner order and
+    unpacking them equals gathering each field; packed hits scatter back to
+    the original ray positions."""
+    import torch
+    from paper_1910_01304_b200.parallel import _exchange_hits, _exchange_rays
+
+    class OneRank:  # all_to_all_single with one rank is a copy
+        @staticmethod
+        def all_to_all_single(out, inp, out_splits, in_splits, group=None):
+            out.copy_(inp)
+
+    rng = np.random.default_rng(7)
+    n = 100003
+    O = torch.from_numpy(rng.normal(size=(n, 3)).astype(np.float32)).cuda()
+    D = torch.from_numpy(rng.normal(size=(n, 3)).astype(np.float32)).cuda()
+    t0 = torch.from_numpy(rng.random(n)).cuda()
+    t1 = t0 + 1.0
+    perm = torch.from_numpy(rng.permutation(n).astype(np.int32)).cuda()
+    Or, Dr, t0r, t1r = _exchange_rays(OneRank, perm, O, D, t0, t1, [n], [n], None)
+    p = perm.long()
+    assert torch.equal(Or, O[p]) and torch.equal(Dr, D[p])
+    assert torch.equal(t0r, t0[p]) and torch.equal(t1r, t1[p])
+    hits = {"found": torch.from_numpy(rng.random(n) < 0.5).cuda(), "t": t0r,
+            "slot": torch.arange(n, dtype=torch.int32, device="cuda"),
+            "leaf": -torch.arange(n, dtype=torch.int32, device="cuda")}
+    out = {}
+    _exchange_hits(OneRank, hits, perm, n, out, [n], [n], None)
+    for k in ("found", "t", "slot", "leaf"):
+        ref = torch.empty_like(hits[k])
+        ref[p] = hits[k]
+        assert torch.equal(out[k], ref), k
