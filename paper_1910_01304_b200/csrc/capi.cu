@@ -244,6 +244,15 @@ __global__ void k_to_host(char* dst, const char* src, int bytes) {
   for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
 }
 __global__ void k_set_i32(int32_t* dst, int32_t v) { *dst = v; }
+// end-of-wave readback into the pinned buffer: meta -> [28, 32), err -> [3],
+// stats -> [4, 20)
+__global__ void k_wave_readback(const long long* meta, const int* err,
+                                const unsigned long long* stats, long long* pin) {
+  const int k = threadIdx.x;
+  if (k < 4) pin[28 + k] = meta[k];
+  if (k == 4) *reinterpret_cast<int*>(pin + 3) = *err;
+  if (stats && k < 16) pin[4 + k] = (long long)stats[k];
+}
 __global__ void k_set_i64(long long* dst, long long v) { *dst = v; }
 
 int to_host(void* pinned_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
@@ -563,10 +572,8 @@ static int read_meta_and_finish(TableDev& t, int* err, cudaStream_t st, Stager& 
                                 unsigned long long* stats_dev) {
   int rc;
   if ((rc = g_pinned.get())) return rc;
-  if ((rc = to_host(g_pinned.p + 28, t.meta, sizeof(long long) * 4, st))) return rc;
-  if ((rc = to_host(g_pinned.p + 3, err, sizeof(int), st))) return rc;
-  if (stats_dev)
-    if ((rc = to_host(g_pinned.p + 4, stats_dev, sizeof(long long) * 16, st))) return rc;
+  k_wave_readback<<<1, 32, 0, st>>>(t.meta, err, stats_dev, g_pinned.p);  // one launch
+  HRPP_LAUNCHED();
   if ((rc = sg.finish())) return rc;
   int e = *(int*)(g_pinned.p + 3);
   if (e == 0) {
@@ -737,9 +744,10 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
   }
   int* err;
   unsigned long long* sdev;
-  if ((rc = ws.get("w_err", 1, &err)) || (rc = ws.get("w_stats", 16, &sdev))) return rc;
-  HRPP_CK(cudaMemsetAsync(err, 0, sizeof(int), st));
-  HRPP_CK(cudaMemsetAsync(sdev, 0, sizeof(unsigned long long) * 16, st));
+  // stats [0, 16) and the error flag (slot 16) in one buffer: one memset
+  if ((rc = ws.get("w_stats", 17, &sdev))) return rc;
+  err = reinterpret_cast<int*>(sdev + 16);
+  HRPP_CK(cudaMemsetAsync(sdev, 0, sizeof(unsigned long long) * 17, st));
   if (mode != HRPP_MODE_BASELINE) {
     if ((rc = launch_hash(dO, dD, n, t->precision, keys, err, st))) return rc;
   }

@@ -149,7 +149,7 @@ struct Segments {
 // lane_bits = 1 + 2p for hash keys (sorted on their 3(1+2p) used bits), 0 for
 // arbitrary 64-bit keys.
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, Segments* seg,
-                 cudaStream_t st);
+                 cudaStream_t st, int* nsegs_mapped = nullptr);
 // indices i < n with flags[i] != 0, ascending, count to *count_dev
 int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, int* count_dev,
                   cudaStream_t st);

@@ -87,6 +87,7 @@ struct ConsultArgs {
   const int32_t* f_box32;  // live: the fallback traversal's counts
   const int32_t* f_tri32;
   const uint8_t* f_known;  // live only
+  uint8_t* f_known_clear;  // live: eval0 zeroes it (one pass fewer)
   // outputs by ray index
   uint8_t* o_found;
   double* o_t;
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, in
     const int32_t i = a.sidx[p];
     const int32_t s = a.seg_id[p] - 1;
     a.seg_of_ray[i] = s;
+    if (a.f_known_clear) a.f_known_clear[i] = 0;
     const int32_t ex_len = a.seg_exlen[s];
     Hit acc = empty_entry_result(CLOSEST);
     if (ex_len > 0) {
@@ -849,12 +851,10 @@ template <bool CLOSEST, bool LIVE, int STACK>
 static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, int64_t nseg_cap) {
   uint8_t *cls, *cls_sorted;
   int32_t *ids, *ids_sorted;
-  int* bounds;
   int rc;
   const int64_t m = nseg_cap > 0 ? nseg_cap : 1;
   if ((rc = ws.get("rg_cls", m, &cls)) || (rc = ws.get("rg_cls2", m, &cls_sorted)) ||
-      (rc = ws.get("rg_ids", m, &ids)) || (rc = ws.get("rg_ids2", m, &ids_sorted)) ||
-      (rc = ws.get("rg_bounds", 16, &bounds)))
+      (rc = ws.get("rg_ids", m, &ids)) || (rc = ws.get("rg_ids2", m, &ids_sorted)))
     return rc;
   k_replay_class<<<grid_for(m, 256, num_sms() * 8), 256, 0, st>>>(a, m, cls, ids);
   HRPP_LAUNCHED();
@@ -864,14 +864,14 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   if ((rc = ws.get_raw("rg_tmp", b, &tmp))) return rc;
   HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 4,
                                           st));
-  k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds);
-  HRPP_LAUNCHED();
   int hb[10];
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
-  if ((rc = to_host(pin + 40, bounds, sizeof(int) * 10, st))) return rc;
+  // bounds written straight into this thread's mapped pinned buffer
+  k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, reinterpret_cast<int*>(pin + 40));
+  HRPP_LAUNCHED();
   HRPP_CK(cudaStreamSynchronize(st));
-  memcpy(hb, pin + 40, sizeof(int) * 10);
+  memcpy(hb, (const void*)(pin + 40), sizeof(int) * 10);
   auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
 #define HRPP_GROUP(K, GS)                                                                      \
   if (cnt(K) > 0) {                                                                            \
@@ -974,12 +974,13 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   const int32_t* anc;
   if ((rc = const_cast<BvhDev&>(b).ancestor_lut(t.go_up, &anc))) return rc;
   Segments seg;
-  if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st))) return rc;
   // new entries <= key segments: read the segment count once so the hash
   // index stays sized to the table (L2-resident for c1-c3 tables), not to the wave
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
-  if ((rc = to_host(pin + 32, seg.nsegs, sizeof(int), st))) return rc;
+  if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st,
+                         reinterpret_cast<int*>(pin + 32))))
+    return rc;
   ConsultArgs a{};
   Workspace& ws = t.ws;
   if ((rc = ws.get("k_segofray", n, &a.seg_of_ray))) return rc;
@@ -1048,7 +1049,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.o_t = c.o_t;
     a.o_slot = c.o_slot;
     a.o_leaf = c.o_leaf;
-    HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
+    a.f_known_clear = f_known;  // zeroed by eval0
     if (rounds > 0) HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));  // else eval0 writes all
     {
       ProfScope ps(P_CONSULT, st);

@@ -77,12 +77,14 @@ __global__ void k_head_flags(const unsigned long long* __restrict__ src, int64_t
   }
 }
 
-__global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n) {
+__global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n,
+                               int* nsegs_mapped) {
   seg_start[*nsegs] = (int32_t)n;
+  if (nsegs_mapped) *nsegs_mapped = *nsegs;  // host-visible (mapped pinned memory)
 }
 
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, Segments* seg,
-                 cudaStream_t st) {
+                 cudaStream_t st, int* nsegs_mapped) {
   int32_t* iota;
   int32_t* flags;
   unsigned long long* packed = nullptr;
@@ -125,7 +127,7 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, 
     HRPP_CK(cub::DeviceSelect::Flagged(tmp, b_sel, cnt, flags, seg->seg_start, seg->nsegs,
                                        (int)n, st));
     HRPP_CK(cub::DeviceScan::InclusiveSum(tmp, b_scan, flags, seg->seg_id, (int)n, st));
-    k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n);
+    k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n, nsegs_mapped);
     HRPP_LAUNCHED();
     return 0;
   }
@@ -160,7 +162,7 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, 
                                      st));
   // seg_id[p] = 1 + index of the key segment holding sorted position p
   HRPP_CK(cub::DeviceScan::InclusiveSum(tmp, b_scan, flags, seg->seg_id, (int)n, st));
-  k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n);
+  k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n, nsegs_mapped);
   HRPP_LAUNCHED();
   return 0;
 }
