@@ -28,19 +28,22 @@ namespace hrpp {
 #ifndef HRPP_OPAQUE_SIGNS
 #define HRPP_OPAQUE_SIGNS 1
 #endif
+// HRPP_BOX32 (default 1): the slab test runs in float32 with a certified
+// error margin and falls back to the reference's float64 test only when the
+// float32 result is within the margin (see box_hit32).  Nodes are stored as
+// 32-B float32 records (the reference's own bmin/bmax values, exact in
+// float64); triangles stay pre-widened float64 (HRPP_NODE_F64).
+#ifndef HRPP_BOX32
+#define HRPP_BOX32 1
+#endif
 
 
 
-#if HRPP_NODE_F64
+#if HRPP_NODE_F64 && !HRPP_BOX32
 struct __align__(16) DNode {  // 64 B: four 16-B loads
   double lo[3], hi[3];
   int32_t a, b;
   int64_t pad;
-};
-struct __align__(16) DTri {  // 80 B: five 16-B loads
-  double v[9];
-  int32_t leaf;  // the leaf node whose slot range holds this slot (-1: none)
-  int32_t pad;
 };
 #else
 struct __align__(16) DNode {  // 32 B: two 16-B loads
@@ -49,6 +52,14 @@ struct __align__(16) DNode {  // 32 B: two 16-B loads
   float bmax[3];
   int32_t b;
 };
+#endif
+#if HRPP_NODE_F64
+struct __align__(16) DTri {  // 80 B: five 16-B loads
+  double v[9];
+  int32_t leaf;  // the leaf node whose slot range holds this slot (-1: none)
+  int32_t pad;
+};
+#else
 struct __align__(16) DTri {  // 48 B: three 16-B loads
   float4 p0, p1, p2;
 };
@@ -57,7 +68,7 @@ struct __align__(16) DTri {  // 48 B: three 16-B loads
 // Host-side packing of the reference's arrays into the device records.
 __host__ __device__ inline void pack_node(DNode& d, const float* lo, const float* hi, int32_t a,
                                           int32_t b) {
-#if HRPP_NODE_F64
+#if HRPP_NODE_F64 && !HRPP_BOX32
   for (int k = 0; k < 3; k++) {
     d.lo[k] = lo[k];
     d.hi[k] = hi[k];
@@ -129,7 +140,7 @@ struct NodeBox {
 
 __device__ __forceinline__ NodeBox load_node(const DNode* __restrict__ nodes, int32_t nd) {
   NodeBox n;
-#if HRPP_NODE_F64
+#if HRPP_NODE_F64 && !HRPP_BOX32
   const double2* p = reinterpret_cast<const double2*>(nodes + nd);
   const double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
   const int4 q3 = __ldg(reinterpret_cast<const int4*>(nodes + nd) + 3);
@@ -238,6 +249,104 @@ __device__ __forceinline__ bool tri_test(const DTri* __restrict__ tris, int32_t 
   return true;
 }
 
+#if HRPP_BOX32
+// The ray as the wave stores it (float32 O and D, exact in float64) plus its
+// float32 slab-test constants; the float64 values the reference computes
+// with are exact widenings of these (o, d) or recomputed on demand (1/d).
+struct Ray {
+  float ox, oy, oz, dx, dy, dz;
+  float ivx, ivy, ivz;  // correctly rounded float32 1/d (signed inf for 0)
+  float t0f;            // float32 tmin
+  float cm;             // margin scale 2^-18; NaN for rays outside the
+                        // certified range (every box test then runs in float64)
+  double tmin, tmax;
+};
+
+// The certified range of box_hit32: every direction component is 0 or has a
+// magnitude in [2^-60, 2^60] (1/d is finite, normal and not near overflow in
+// float32), the origin is finite with magnitude < 2^60, tmin/tmax not NaN.
+__device__ __forceinline__ bool dir_ok32(float d) {
+  const float a = fabsf(d);
+  return d == 0.0f || (a >= 0x1p-60f && a <= 0x1p60f);
+}
+
+__device__ __forceinline__ Ray make_ray(const float* __restrict__ O, const float* __restrict__ D,
+                                        const double* __restrict__ tmin,
+                                        const double* __restrict__ tmax, int64_t i) {
+  Ray r;
+  r.ox = O[3 * i]; r.oy = O[3 * i + 1]; r.oz = O[3 * i + 2];
+  r.dx = D[3 * i]; r.dy = D[3 * i + 1]; r.dz = D[3 * i + 2];
+  r.ivx = __frcp_rn(r.dx); r.ivy = __frcp_rn(r.dy); r.ivz = __frcp_rn(r.dz);
+  r.tmin = tmin[i];
+  r.tmax = tmax[i];
+  r.t0f = (float)r.tmin;
+  const bool ok = dir_ok32(r.dx) && dir_ok32(r.dy) && dir_ok32(r.dz) &&
+                  fabsf(r.ox) < 0x1p60f && fabsf(r.oy) < 0x1p60f && fabsf(r.oz) < 0x1p60f &&
+                  r.tmin == r.tmin && r.tmax == r.tmax;
+  r.cm = ok ? 0x1p-18f : __int_as_float(0x7fffffff);
+  return r;
+}
+
+struct NodeBox32 {
+  float lx, ly, lz, hx, hy, hz;
+  int32_t a, b;
+};
+
+__device__ __forceinline__ NodeBox32 load_node32(const DNode* __restrict__ nodes, int32_t nd) {
+  const float4* p = reinterpret_cast<const float4*>(nodes + nd);
+  const float4 lo = __ldg(p), hi = __ldg(p + 1);
+  NodeBox32 n;
+  n.lx = lo.x; n.ly = lo.y; n.lz = lo.z; n.hx = hi.x; n.hy = hi.y; n.hz = hi.z;
+  n.a = __float_as_int(lo.w);
+  n.b = __float_as_int(hi.w);
+  return n;
+}
+
+// The reference's float64 slab test (hrpp/kernels.py:23-51) on the same
+// node and ray, every float64 value rebuilt exactly (widenings of the
+// float32 inputs, 1/d recomputed as the reference does).  Out of line: it
+// runs only for the rare box tests box_hit32 cannot certify.
+static __device__ __noinline__ bool box_hit_exact(float lx, float ly, float lz, float hx, float hy,
+                                           float hz, float ox, float oy, float oz, float dx,
+                                           float dy, float dz, double t0, double t1) {
+  NodeBox n;
+  n.lx = lx; n.ly = ly; n.lz = lz; n.hx = hx; n.hy = hy; n.hz = hz;
+  return box_hit(n, ox, oy, oz, recip(dx), recip(dy), recip(dz), t0, t1);
+}
+
+// Slab test in float32 with a certified decision.
+//
+// For a ray in the certified range each float32 slab value a = (lo - o) * iv
+// is within 3u|a| (u = 2^-24: one rounding in the subtraction of exact
+// float32 inputs, one in the correctly rounded reciprocal, one in the
+// product) of the real value, and the reference's float64 value within
+// 3*2^-53|a|; infinities and NaNs (zero direction components) arise
+// identically in both.  max/min of such values keep the bound relative to
+// the result, so with tn, tf the float32 entry/exit and s = |tn| + |tf|:
+//   |(tf - tn) - (tf64 - tn64)| <= ~4u s + 2^-149 (underflow)  <  m,
+//   m = 2^-18 s + 2^-126.
+// So d = tf - tn > m certifies tn64 <= tf64 (hit) and d < -m certifies a
+// miss; anything else -- including every inf/NaN in d or m, and every test
+// of a ray outside the certified range (cm = NaN) -- is decided by the
+// float64 test.  The result is therefore always the reference's.
+__device__ __forceinline__ bool box_hit32(const NodeBox32& n, const Ray& r, uint32_t ivneg,
+                                          float t1f, double t1) {
+  const float nx = (ivneg & 1u) ? n.hx : n.lx, fx = (ivneg & 1u) ? n.lx : n.hx;
+  const float ny = (ivneg & 2u) ? n.hy : n.ly, fy = (ivneg & 2u) ? n.ly : n.hy;
+  const float nz = (ivneg & 4u) ? n.hz : n.lz, fz = (ivneg & 4u) ? n.lz : n.hz;
+  const float ax = (nx - r.ox) * r.ivx, bx = (fx - r.ox) * r.ivx;
+  const float ay = (ny - r.oy) * r.ivy, by = (fy - r.oy) * r.ivy;
+  const float az = (nz - r.oz) * r.ivz, bz = (fz - r.oz) * r.ivz;
+  const float tn = fmaxf(fmaxf(r.t0f, ax), fmaxf(ay, az));
+  const float tf = fminf(fminf(t1f, bx), fminf(by, bz));
+  const float d = tf - tn;
+  const float m = __fmaf_ru(fabsf(tn) + fabsf(tf), r.cm, 0x1p-126f);
+  if (d > m) return true;
+  if (d < -m) return false;
+  return box_hit_exact(n.lx, n.ly, n.lz, n.hx, n.hy, n.hz, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz,
+                       r.tmin, t1);
+}
+#else
 struct Ray {
   double ox, oy, oz, dx, dy, dz, ivx, ivy, ivz, tmin, tmax;
 };
@@ -254,6 +363,7 @@ __device__ __forceinline__ Ray make_ray(const float* __restrict__ O, const float
   r.tmax = tmax[i];
   return r;
 }
+#endif
 
 // Per-thread traversal stack in local memory.  (A shared-memory column per
 // thread measured 8-15 % slower: it takes L1 capacity from the node reads.)
@@ -279,10 +389,17 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   int top = 0;
   int32_t nd = start;
   // d[axis] < 0 per axis (bit axis): the near child is the right one
+#if HRPP_BOX32
+  const uint32_t dneg = (r.dx >= 0.0f ? 0u : 1u) | (r.dy >= 0.0f ? 0u : 2u) |
+                        (r.dz >= 0.0f ? 0u : 4u);
+  uint32_t ivneg = (r.ivx < 0.0f ? 1u : 0u) | (r.ivy < 0.0f ? 2u : 0u) |
+                   (r.ivz < 0.0f ? 4u : 0u);
+#else
   const uint32_t dneg = (r.dx >= 0.0 ? 0u : 1u) | (r.dy >= 0.0 ? 0u : 2u) |
                         (r.dz >= 0.0 ? 0u : 4u);
   uint32_t ivneg = (r.ivx < 0.0 ? 1u : 0u) | (r.ivy < 0.0 ? 2u : 0u) |
                    (r.ivz < 0.0 ? 4u : 0u);
+#endif
 #if HRPP_OPAQUE_SIGNS
   asm volatile("mov.u32 %0, %0;" : "+r"(ivneg));  // keep the bits, not 3 float64 compares
 #endif
@@ -295,10 +412,18 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   h.slot = -1;
   h.boxes = 0;
   h.tris = 0;
+#if HRPP_BOX32
+  float t1f = (float)h.t;  // float32 copy of the interval end for box_hit32
+#endif
   for (;;) {
     h.boxes++;
+#if HRPP_BOX32
+    const NodeBox32 nb = load_node32(nodes, nd);
+    if (box_hit32(nb, r, ivneg, t1f, h.t)) {
+#else
     const NodeBox nb = load_node(nodes, nd);
     if (box_hit_s(nb, r.ox, r.oy, r.oz, r.ivx, r.ivy, r.ivz, ivneg, r.tmin, h.t)) {
+#endif
       const int32_t a = nb.a;
       const int32_t b = nb.b;
       if (a >= 0) {
@@ -316,6 +441,9 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         if (tri_test(tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) && t >= r.tmin &&
             (h.slot < 0 ? t <= h.t : t < h.t)) {
           h.t = t;
+#if HRPP_BOX32
+          t1f = (float)t;
+#endif
           h.slot = k;
           if (!CLOSEST) {
             top = 0;

@@ -276,7 +276,7 @@ struct TraceArgs {
 // shadow, +13 % bounce over the uncapped 86).  A leaf-batched "while-while"
 // loop (warp-synchronous box and triangle phases) measured 40 % slower.
 #ifndef HRPP_TRACE_MINB
-#define HRPP_TRACE_MINB 7
+#define HRPP_TRACE_MINB 8
 #endif
 
 template <bool CLOSEST, int STACK>

@@ -174,6 +174,71 @@ def test_trace_vs_oracle_spheres_random(hb, oracle_mod):
             assert np.array_equal(got[k], v), (closest, k)
 
 
+def _adversarial_rays(b, n, seed):
+    """Rays built to sit on the float32 slab test's decision boundaries:
+    origins on node planes, directions through node corners, zero / signed
+    zero / tiny / denormal / huge direction components, extreme and NaN
+    tmin/tmax, huge origins (outside the float32 certified range)."""
+    rng = np.random.default_rng(seed)
+    nn = b.bmin.shape[0]
+    nd = rng.integers(0, nn, n)
+    lo, hi = b.bmin[nd].astype(np.float32), b.bmax[nd].astype(np.float32)
+    pick = rng.integers(0, 2, (n, 3)).astype(bool)
+    corner = np.where(pick, lo, hi)
+    O = rng.uniform(-6, 6, (n, 3)).astype(np.float32)
+    q = n // 4
+    # a quarter: origin on one of the node's planes
+    ax = rng.integers(0, 3, q)
+    O[np.arange(q), ax] = np.where(rng.integers(0, 2, q) == 1, lo[np.arange(q), ax],
+                                   hi[np.arange(q), ax])
+    D = (corner - O).astype(np.float32)  # through a node corner
+    D[q:2 * q] = rng.normal(size=(q, 3)).astype(np.float32)
+    special = np.array([0.0, -0.0, 1e-30, -1e-30, 1e-40, 2.0 ** -61, 2.0 ** -59, -2.0 ** -60,
+                        1e20, -2.0 ** 61, 2.0 ** 60, 1.0], np.float32)
+    m = rng.random((n, 3)) < 0.15
+    D[m] = special[rng.integers(0, special.size, int(m.sum()))]
+    O[rng.random((n, 3)) < 0.002] = np.float32(2.0 ** 61)  # outside the certified range
+    tmin = np.zeros(n)
+    tmax = np.full(n, np.inf)
+    r = rng.random(n)
+    tmin[r < 0.05] = -1.0
+    tmin[(r >= 0.05) & (r < 0.08)] = np.nan
+    tmax[(r >= 0.08) & (r < 0.11)] = np.nan
+    tmax[(r >= 0.11) & (r < 0.2)] = 1e300
+    tmax[(r >= 0.2) & (r < 0.3)] = rng.uniform(0.0, 3.0, int(((r >= 0.2) & (r < 0.3)).sum()))
+    sel = (r >= 0.3) & (r < 0.33)
+    tmax[sel] = 1e-300
+    sel = (r >= 0.33) & (r < 0.36)
+    tmin[sel] = 1.0
+    tmax[sel] = 1.0
+    return O, D, tmin, tmax
+
+
+@pytest.mark.parametrize("scene", ["spheres", "strip8", "c1"])
+def test_trace_box_boundaries_vs_oracle(hb, oracle_mod, scene):
+    """The float32 slab test with float64 fallback (hrpp_device.cuh
+    box_hit32) decides every box exactly as the reference's float64 test:
+    all outputs and counters equal the oracle on boundary-seeking rays."""
+    from oracle.oracle import OracleBvh
+    if scene == "c1":
+        from paper_1910_01304_b200 import scenes
+        sc = scenes.make_scene("c1", resolution=(32, 32))
+        b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
+        ob = OracleBvh(b.bmin, b.bmax, b.left, b.right, b.axis, b.first, b.count, b.parent,
+                       b.depth, b.tv0, b.tv1, b.tv2, b.tri_ids)
+    else:
+        g = load_golden(f"bvh_{scene}.npz")
+        b = gbvh(hb, scene)
+        ob = OracleBvh.from_dict(g)
+    O, D, tmin, tmax = _adversarial_rays(b, 60_000, seed=11)
+    for closest in (True, False):
+        got = (hb.intersect_closest_batch if closest else hb.intersect_any_batch)(
+            b, O, D, tmin, tmax)
+        ref = ob.trace_batch(closest, O, D, tmin, tmax)
+        for k, v in ref.items():
+            assert np.array_equal(got[k], v, equal_nan=True), (scene, closest, k)
+
+
 # -- the wave (limit / live / baseline) ----------------------------------------------
 
 @pytest.mark.parametrize("p,g_", SETTINGS)
