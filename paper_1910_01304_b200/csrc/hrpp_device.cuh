@@ -55,7 +55,9 @@ struct __align__(16) DNode {  // 32 B: two 16-B loads
 #endif
 #if HRPP_NODE_F64
 struct __align__(16) DTri {  // 80 B: five 16-B loads
-  double v[9];
+  double v[9];  // v0, then the edges e1 = v1 - v0, e2 = v2 - v0 in float64
+                // (hrpp/kernels.py:60-65; the same rounding the reference does
+                // per test, done once when the BVH is created)
   int32_t leaf;  // the leaf node whose slot range holds this slot (-1: none)
   int32_t pad;
 };
@@ -91,8 +93,8 @@ __host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b
 #if HRPP_NODE_F64
   for (int k = 0; k < 3; k++) {
     t.v[k] = a[k];
-    t.v[3 + k] = b[k];
-    t.v[6 + k] = c[k];
+    t.v[3 + k] = (double)b[k] - (double)a[k];
+    t.v[6 + k] = (double)c[k] - (double)a[k];
   }
   t.leaf = leaf;
   t.pad = 0;
@@ -204,7 +206,7 @@ __device__ __forceinline__ bool box_hit_s(const NodeBox& n, double ox, double oy
   return tn <= tf;
 }
 
-// Triangle vertices widened to float64 (exact).
+// Triangle v0 and edges e1, e2 in float64 (the reference's values).
 __device__ __forceinline__ void load_tri(const DTri* __restrict__ tris, int32_t k, double v[9]) {
 #if HRPP_NODE_F64
   const double2* p = reinterpret_cast<const double2*>(tris + k);
@@ -217,6 +219,7 @@ __device__ __forceinline__ void load_tri(const DTri* __restrict__ tris, int32_t 
   const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
   v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w; v[4] = q1.x; v[5] = q1.y;
   v[6] = q1.z; v[7] = q1.w; v[8] = q2.x;
+  for (int k = 3; k < 9; k++) v[k] -= v[k % 3];
 #endif
 }
 
@@ -227,8 +230,8 @@ __device__ __forceinline__ bool tri_test(const DTri* __restrict__ tris, int32_t 
   double q[9];
   load_tri(tris, k, q);
   double ax = q[0], ay = q[1], az = q[2];
-  double e1x = q[3] - ax, e1y = q[4] - ay, e1z = q[5] - az;
-  double e2x = q[6] - ax, e2y = q[7] - ay, e2z = q[8] - az;
+  double e1x = q[3], e1y = q[4], e1z = q[5];
+  double e2x = q[6], e2y = q[7], e2z = q[8];
   double px = dy * e2z - dz * e2y;
   double py = dz * e2x - dx * e2z;
   double pz = dx * e2y - dy * e2x;
@@ -256,9 +259,8 @@ __device__ __forceinline__ bool tri_test(const DTri* __restrict__ tris, int32_t 
 struct Ray {
   float ox, oy, oz, dx, dy, dz;
   float ivx, ivy, ivz;  // correctly rounded float32 1/d (signed inf for 0)
-  float t0f;            // float32 tmin
-  float cm;             // margin scale 2^-18; NaN for rays outside the
-                        // certified range (every box test then runs in float64)
+  float t0f;            // float32 tmin; +inf for rays outside the certified
+                        // range (tn = +inf: every box test then runs in float64)
   double tmin, tmax;
 };
 
@@ -279,11 +281,10 @@ __device__ __forceinline__ Ray make_ray(const float* __restrict__ O, const float
   r.ivx = __frcp_rn(r.dx); r.ivy = __frcp_rn(r.dy); r.ivz = __frcp_rn(r.dz);
   r.tmin = tmin[i];
   r.tmax = tmax[i];
-  r.t0f = (float)r.tmin;
   const bool ok = dir_ok32(r.dx) && dir_ok32(r.dy) && dir_ok32(r.dz) &&
                   fabsf(r.ox) < 0x1p60f && fabsf(r.oy) < 0x1p60f && fabsf(r.oz) < 0x1p60f &&
                   r.tmin == r.tmin && r.tmax == r.tmax;
-  r.cm = ok ? 0x1p-18f : __int_as_float(0x7fffffff);
+  r.t0f = ok ? (float)r.tmin : __int_as_float(0x7f800000);
   return r;
 }
 
@@ -327,7 +328,8 @@ static __device__ __noinline__ bool box_hit_exact(float lx, float ly, float lz, 
 //   m = 2^-18 s + 2^-126.
 // So d = tf - tn > m certifies tn64 <= tf64 (hit) and d < -m certifies a
 // miss; anything else -- including every inf/NaN in d or m, and every test
-// of a ray outside the certified range (cm = NaN) -- is decided by the
+// of a ray outside the certified range (t0f = +inf makes tn = +inf, so d is
+// -inf or NaN and m is inf or NaN) -- is decided by the
 // float64 test.  The result is therefore always the reference's.
 __device__ __forceinline__ bool box_hit32(const NodeBox32& n, const Ray& r, uint32_t ivneg,
                                           float t1f, double t1) {
@@ -340,7 +342,7 @@ __device__ __forceinline__ bool box_hit32(const NodeBox32& n, const Ray& r, uint
   const float tn = fmaxf(fmaxf(r.t0f, ax), fmaxf(ay, az));
   const float tf = fminf(fminf(t1f, bx), fminf(by, bz));
   const float d = tf - tn;
-  const float m = __fmaf_ru(fabsf(tn) + fabsf(tf), r.cm, 0x1p-126f);
+  const float m = __fmaf_ru(fabsf(tn) + fabsf(tf), 0x1p-18f, 0x1p-126f);
   if (d > m) return true;
   if (d < -m) return false;
   return box_hit_exact(n.lx, n.ly, n.lz, n.hx, n.hy, n.hz, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz,
@@ -390,10 +392,10 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   int32_t nd = start;
   // d[axis] < 0 per axis (bit axis): the near child is the right one
 #if HRPP_BOX32
-  const uint32_t dneg = (r.dx >= 0.0f ? 0u : 1u) | (r.dy >= 0.0f ? 0u : 2u) |
-                        (r.dz >= 0.0f ? 0u : 4u);
+  // bits 0-2: 1/d < 0 per axis (slab swap); bits 3-5: d < 0 (near child right)
   uint32_t ivneg = (r.ivx < 0.0f ? 1u : 0u) | (r.ivy < 0.0f ? 2u : 0u) |
-                   (r.ivz < 0.0f ? 4u : 0u);
+                   (r.ivz < 0.0f ? 4u : 0u) | (r.dx >= 0.0f ? 0u : 8u) |
+                   (r.dy >= 0.0f ? 0u : 16u) | (r.dz >= 0.0f ? 0u : 32u);
 #else
   const uint32_t dneg = (r.dx >= 0.0 ? 0u : 1u) | (r.dy >= 0.0 ? 0u : 2u) |
                         (r.dz >= 0.0 ? 0u : 4u);
@@ -429,16 +431,34 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
       if (a >= 0) {
         const uint32_t axis = (uint32_t)b >> 30;
         const int32_t right = b & 0x3FFFFFFF;
+#if HRPP_BOX32
+        const bool go_right = (ivneg >> (axis + 3)) & 1u;
+#else
         const bool go_right = (dneg >> axis) & 1u;
+#endif
         stack[top++] = go_right ? a : right;  // far
         nd = go_right ? right : a;             // near, visited next
         continue;
       }
       const int32_t f = ~a, e = f + b;
+#pragma unroll 1
       for (int32_t k = f; k < e; k++) {
         double t, u, v;
         h.tris++;
+#if HRPP_BOX32
+        // widen the ray inside the leaf loop (opaque, so the compiler does not
+        // keep float64 copies of o and d live across the whole traversal)
+        float fo[3] = {r.ox, r.oy, r.oz}, fd[3] = {r.dx, r.dy, r.dz};
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          asm volatile("mov.b32 %0, %0;" : "+f"(fo[c]));
+          asm volatile("mov.b32 %0, %0;" : "+f"(fd[c]));
+        }
+        if (tri_test(tris, k, fo[0], fo[1], fo[2], fd[0], fd[1], fd[2], t, u, v) &&
+            t >= r.tmin &&
+#else
         if (tri_test(tris, k, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, t, u, v) && t >= r.tmin &&
+#endif
             (h.slot < 0 ? t <= h.t : t < h.t)) {
           h.t = t;
 #if HRPP_BOX32

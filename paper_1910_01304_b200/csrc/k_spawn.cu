@@ -116,14 +116,10 @@ __global__ void k_spawn(SpawnArgs a) {
     // geometric normal of the slot (Bvh.slot_normals, hrpp/bvh.py:130-138)
     double q[9];
     load_tri(a.tris, a.slot[i], q);
-    const double v0[3] = {q[0], q[1], q[2]};
-    const double v1[3] = {q[3], q[4], q[5]};
-    const double v2[3] = {q[6], q[7], q[8]};
-    double e1[3], e2[3], N[3];
-    for (int k = 0; k < 3; k++) {
-      e1[k] = v1[k] - v0[k];
-      e2[k] = v2[k] - v0[k];
-    }
+    // q = v0, e1 = v1 - v0, e2 = v2 - v0 (float64, as load_tri returns them)
+    const double e1[3] = {q[3], q[4], q[5]};
+    const double e2[3] = {q[6], q[7], q[8]};
+    double N[3];
     N[0] = e1[1] * e2[2] - e1[2] * e2[1];
     N[1] = e1[2] * e2[0] - e1[0] * e2[2];
     N[2] = e1[0] * e2[1] - e1[1] * e2[0];
