@@ -57,12 +57,26 @@ def main():
         return float(np.median(ts))
 
     ms_c = timeit(lambda: hb.intersect_closest_batch(b, Ot, Dt, t0, t1))
+    import hashlib
+
+    def digest(res):
+        m = hashlib.md5()
+        for k in sorted(res):
+            v = res[k]
+            v = v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)
+            m.update(k.encode())
+            m.update(np.ascontiguousarray(v).tobytes())
+        return m.hexdigest()[:10]
+
+    dig = "-".join(digest(f()) for f in (
+        lambda: hb.intersect_closest_batch(b, Ot, Dt, t0, t1),
+        lambda: hb.intersect_any_batch(b, *S), lambda: hb.intersect_closest_batch(b, *B)))
     ms_a = timeit(lambda: hb.intersect_any_batch(b, *S))
     ms_b = timeit(lambda: hb.intersect_closest_batch(b, *B))
     print(json.dumps({"closest_ms": round(ms_c, 4), "closest_mrays_s": round(n / ms_c / 1e3, 1),
                       "any_ms": round(ms_a, 4), "any_mrays_s": round(len(so) / ms_a / 1e3, 1),
                       "bounce_ms": round(ms_b, 4), "bounce_mrays_s": round(len(bo) / ms_b / 1e3, 1),
-                      "mean_box": float(base["box"].mean()), "n": n}))
+                      "mean_box": float(base["box"].mean()), "n": n, "digest": dig}))
 
 
 if __name__ == "__main__":
