@@ -348,7 +348,9 @@ __global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, in
       catch_up<CLOSEST, STACK>(a, r, acc, 0, ex_len, a.seg_exoff[s], ex_len, nullptr);
     }
     if (ex_len > 0 || !a.sparse_state) store_state(a, i, acc, ex_len);
-    if (mark_need) a.need[i] = !(ex_len > 0 && acc.found);
+    // need[] is preset to 1 (coalesced memset): only the wave-start TPs,
+    // rare, are cleared here with a scattered store
+    if (mark_need && ex_len > 0 && acc.found) a.need[i] = 0;
   }
 }
 
@@ -1049,8 +1051,10 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.o_t = c.o_t;
     a.o_slot = c.o_slot;
     a.o_leaf = c.o_leaf;
-    a.f_known_clear = f_known;  // zeroed by eval0
-    if (rounds > 0) HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));  // else eval0 writes all
+    // coalesced presets instead of two scattered byte stores per ray in eval0
+    a.f_known_clear = nullptr;
+    HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
+    HRPP_CK(cudaMemsetAsync(a.need, rounds > 0 ? 0 : 1, n, st));  // eval0 clears the TPs
     {
       ProfScope ps(P_CONSULT, st);
       if (t.closest) dispatch_eval0<true>(b.stack, grid, st, a, n, rounds == 0);
