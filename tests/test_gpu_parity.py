@@ -214,16 +214,24 @@ def _adversarial_rays(b, n, seed):
     return O, D, tmin, tmax
 
 
-@pytest.mark.parametrize("scene", ["spheres", "strip8", "c1"])
+@pytest.mark.parametrize("scene", ["spheres", "strip8", "c1", "c1x2^100", "c1x2^-100"])
 def test_trace_box_boundaries_vs_oracle(hb, oracle_mod, scene):
     """The float32 slab test with float64 fallback (hrpp_device.cuh
     box_hit32) decides every box exactly as the reference's float64 test:
-    all outputs and counters equal the oracle on boundary-seeking rays."""
+    all outputs and counters equal the oracle on boundary-seeking rays, also
+    on the c1 BVH scaled (exactly, by a power of two) towards float32
+    overflow and underflow, where slab values with the huge / tiny direction
+    components leave the float32 range or fall below its normal range."""
     from oracle.oracle import OracleBvh
-    if scene == "c1":
+    if scene.startswith("c1"):
         from paper_1910_01304_b200 import scenes
         sc = scenes.make_scene("c1", resolution=(32, 32))
         b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
+        if "x" in scene:
+            k = np.float32(2.0 ** int(scene.split("^")[1]))
+            b = hb.Bvh(b.bmin * k, b.bmax * k, b.left, b.right, b.axis, b.first, b.count,
+                       b.parent, b.depth, b.tv0 * k, b.tv1 * k, b.tv2 * k, b.tri_ids,
+                       int(b.depth.max()))
         ob = OracleBvh(b.bmin, b.bmax, b.left, b.right, b.axis, b.first, b.count, b.parent,
                        b.depth, b.tv0, b.tv1, b.tv2, b.tri_ids)
     else:
@@ -231,6 +239,12 @@ def test_trace_box_boundaries_vs_oracle(hb, oracle_mod, scene):
         b = gbvh(hb, scene)
         ob = OracleBvh.from_dict(g)
     O, D, tmin, tmax = _adversarial_rays(b, 60_000, seed=11)
+    if "x" in scene:  # free origins and finite intervals at the scene's scale
+        k = 2.0 ** int(scene.split("^")[1])
+        free = ~np.isin(O, b.bmin) & ~np.isin(O, b.bmax) & (np.abs(O) < 1e6)
+        O = np.where(free, O * np.float32(k), O).astype(np.float32)
+        fin = np.isfinite(tmax) & (tmax > 1e-200) & (tmax < 1e200)
+        tmax = np.where(fin, tmax * k, tmax)
     for closest in (True, False):
         got = (hb.intersect_closest_batch if closest else hb.intersect_any_batch)(
             b, O, D, tmin, tmax)
