@@ -849,6 +849,34 @@ static int launch_replay(bool closest, bool live, int stack, cudaStream_t st,
 }
 
 // All full results known: replay every length class with its own group size.
+#ifndef HRPP_REPLAY_STREAMS
+#define HRPP_REPLAY_STREAMS 8
+#endif
+
+// Per host thread and device: side streams (and fork/join events) for the
+// concurrent replay classes.
+struct SidePool {
+  cudaStream_t s[8];
+  cudaEvent_t fork, join[8];
+};
+
+static SidePool& side_pool() {
+  thread_local std::map<int, SidePool> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = pools.find(dev);
+  if (it == pools.end()) {
+    SidePool p;
+    for (int k = 0; k < 8; k++) {
+      cudaStreamCreateWithFlags(&p.s[k], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&p.join[k], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
+    it = pools.emplace(dev, p).first;
+  }
+  return it->second;
+}
+
 template <bool CLOSEST, bool LIVE, int STACK>
 static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, int64_t nseg_cap) {
   uint8_t *cls, *cls_sorted;
@@ -875,10 +903,23 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   HRPP_CK(cudaStreamSynchronize(st));
   memcpy(hb, (const void*)(pin + 40), sizeof(int) * 10);
   auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
+  // The classes hold disjoint segments, so their kernels run concurrently:
+  // each is small and latency-bound (a few hundred blocks, or one long
+  // chain per segment), and back to back each one's tail idled the GPU.
+  SidePool& sp = side_pool();
+  HRPP_CK(cudaEventRecord(sp.fork, st));
+  int used = 0;
+  auto side = [&](int k) -> cudaStream_t {
+    if (HRPP_REPLAY_STREAMS <= 1) return st;
+    cudaStream_t s2 = sp.s[k % HRPP_REPLAY_STREAMS];
+    if (!(used & (1 << (k % HRPP_REPLAY_STREAMS)))) cudaStreamWaitEvent(s2, sp.fork, 0);
+    used |= 1 << (k % HRPP_REPLAY_STREAMS);
+    return s2;
+  };
 #define HRPP_GROUP(K, GS)                                                                      \
   if (cnt(K) > 0) {                                                                            \
     const int64_t thr = (int64_t)cnt(K) * GS;                                                  \
-    k_replay_group<CLOSEST, LIVE, STACK, GS><<<(int)((thr + 127) / 128), 128, 0, st>>>(       \
+    k_replay_group<CLOSEST, LIVE, STACK, GS><<<(int)((thr + 127) / 128), 128, 0, side(K)>>>(  \
         a, ids_sorted + hb[K], cnt(K));                                                        \
     HRPP_LAUNCHED();                                                                           \
   }
@@ -890,10 +931,16 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   HRPP_GROUP(6, 32)
 #undef HRPP_GROUP
   if (cnt(7) > 0) {  // long segments: a warp each, 32-ray tiles
-    k_replay_block<CLOSEST, LIVE, STACK, 32><<<cnt(7), 32, 0, st>>>(a, ids_sorted + hb[7],
-                                                                      cnt(7));
+    k_replay_block<CLOSEST, LIVE, STACK, 32><<<cnt(7), 32, 0, side(7)>>>(a, ids_sorted + hb[7],
+                                                                           cnt(7));
     HRPP_LAUNCHED();
   }
+  // class 8 below runs on st after the join (it sorts by remaining length)
+  for (int k = 0; k < HRPP_REPLAY_STREAMS; k++)
+    if (used & (1 << k)) {
+      HRPP_CK(cudaEventRecord(sp.join[k], sp.s[k]));
+      HRPP_CK(cudaStreamWaitEvent(st, sp.join[k], 0));
+    }
   if (cnt(8) > 0) {  // very long segments: a whole block each, longest first
     const int c8 = cnt(8);
     int32_t *rem, *rem2, *ids8;
