@@ -639,9 +639,12 @@ constexpr int kBlockReplayMin = 1024;
 #ifndef HRPP_BLOCK_MINB
 #define HRPP_BLOCK_MINB 2
 #endif
+#ifndef HRPP_BLOCK32_MINB
+#define HRPP_BLOCK32_MINB 32  // warp-per-segment replay: 32-thread blocks per SM
+#endif
 
 template <bool CLOSEST, bool LIVE, int STACK, int BS>
-__global__ void __launch_bounds__(BS, BS == 32 ? 16 : HRPP_BLOCK_MINB)
+__global__ void __launch_bounds__(BS, BS == 32 ? HRPP_BLOCK32_MINB : HRPP_BLOCK_MINB)
     k_replay_block(ConsultArgs a, const int32_t* list, int count) {
   if (*a.err) return;
   __shared__ int s_f;
