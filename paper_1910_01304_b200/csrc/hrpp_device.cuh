@@ -36,6 +36,9 @@ namespace hrpp {
 #ifndef HRPP_BOX32
 #define HRPP_BOX32 1
 #endif
+#ifndef HRPP_LDG256
+#define HRPP_LDG256 1
+#endif
 
 
 
@@ -293,13 +296,24 @@ struct NodeBox32 {
   int32_t a, b;
 };
 
+// One 256-bit load per node (sm_100 LDG.E.ENL2.256; records are 32-B aligned).
 __device__ __forceinline__ NodeBox32 load_node32(const DNode* __restrict__ nodes, int32_t nd) {
+  NodeBox32 n;
+#if HRPP_LDG256
+  float aw, bw;
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(n.lx), "=f"(n.ly), "=f"(n.lz), "=f"(aw), "=f"(n.hx), "=f"(n.hy), "=f"(n.hz),
+        "=f"(bw)
+      : "l"(nodes + nd));
+  n.a = __float_as_int(aw);
+  n.b = __float_as_int(bw);
+#else
   const float4* p = reinterpret_cast<const float4*>(nodes + nd);
   const float4 lo = __ldg(p), hi = __ldg(p + 1);
-  NodeBox32 n;
   n.lx = lo.x; n.ly = lo.y; n.lz = lo.z; n.hx = hi.x; n.hy = hi.y; n.hz = hi.z;
   n.a = __float_as_int(lo.w);
   n.b = __float_as_int(hi.w);
+#endif
   return n;
 }
 
