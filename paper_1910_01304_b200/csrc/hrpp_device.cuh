@@ -57,12 +57,12 @@ struct __align__(16) DNode {  // 32 B: two 16-B loads
 };
 #endif
 #if HRPP_NODE_F64
-struct __align__(16) DTri {  // 80 B: five 16-B loads
+struct __align__(32) DTri {  // 96 B: three 32-B loads
   double v[9];  // v0, then the edges e1 = v1 - v0, e2 = v2 - v0 in float64
                 // (hrpp/kernels.py:60-65; the same rounding the reference does
                 // per test, done once when the BVH is created)
   int32_t leaf;  // the leaf node whose slot range holds this slot (-1: none)
-  int32_t pad;
+  int32_t pad[5];
 };
 #else
 struct __align__(16) DTri {  // 48 B: three 16-B loads
@@ -100,7 +100,7 @@ __host__ __device__ inline void pack_tri(DTri& t, const float* a, const float* b
     t.v[6 + k] = (double)c[k] - (double)a[k];
   }
   t.leaf = leaf;
-  t.pad = 0;
+  for (int k = 0; k < 5; k++) t.pad[k] = 0;
 #else
   t.p0 = make_float4(a[0], a[1], a[2], b[0]);
   t.p1 = make_float4(b[1], b[2], c[0], c[1]);
@@ -212,11 +212,14 @@ __device__ __forceinline__ bool box_hit_s(const NodeBox& n, double ox, double oy
 // Triangle v0 and edges e1, e2 in float64 (the reference's values).
 __device__ __forceinline__ void load_tri(const DTri* __restrict__ tris, int32_t k, double v[9]) {
 #if HRPP_NODE_F64
-  const double2* p = reinterpret_cast<const double2*>(tris + k);
-  const double2 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
-  const double q4 = __ldg(reinterpret_cast<const double*>(tris + k) + 8);
-  v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y; v[4] = q2.x; v[5] = q2.y;
-  v[6] = q3.x; v[7] = q3.y; v[8] = q4;
+  const double* p = reinterpret_cast<const double*>(tris + k);
+  double w;  // the leaf / pad word
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7]) : "l"(p + 4));
+  v[8] = __ldg(p + 8);
+  (void)w;
 #else
   const float4* p = reinterpret_cast<const float4*>(tris + k);
   const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
