@@ -140,7 +140,7 @@ int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
 
 // Group a batch of keys: stable sort (key, ray) and find key segments.
 struct Segments {
-  unsigned long long* skeys = nullptr;
+  unsigned long long* skeys = nullptr;  // 48-bit keys; valid at segment heads
   int32_t* sidx = nullptr;
   int32_t* seg_start = nullptr;  // nsegs + 1 entries (device count)
   int* nsegs = nullptr;          // device scalar

@@ -77,6 +77,72 @@ __global__ void k_head_flags(const unsigned long long* __restrict__ src, int64_t
   }
 }
 
+// Segment construction fused into one scan over the sorted words: the scan
+// input is the head flag of each sorted position (its key differs from the
+// previous one), the inclusive sum is the segment id (+1), and the output
+// iterator writes seg_id[p], sidx[p] and, at segment heads, seg_start and the
+// unpacked 48-bit key skeys[p] (read only at heads).  Replaces a head-flag
+// pass, a flagged select and a separate scan.
+struct HeadFlag {
+  const unsigned long long* w;
+  int ib;
+  __host__ __device__ __forceinline__ int operator()(int64_t p) const {
+    return p == 0 || (w[p] >> ib) != (w[p - 1] >> ib);
+  }
+};
+
+struct SegWriter {
+  using value_type = int;
+  using difference_type = std::ptrdiff_t;
+  using pointer = void;
+  using iterator_category = std::random_access_iterator_tag;
+  const unsigned long long* w;
+  int ib, b;
+  int64_t base;
+  int32_t* seg_id;
+  int32_t* seg_start;
+  unsigned long long* skeys;
+  int32_t* sidx;
+  struct Ref {
+    const unsigned long long* w;
+    int ib, b;
+    int64_t p;
+    int32_t* seg_id;
+    int32_t* seg_start;
+    unsigned long long* skeys;
+    int32_t* sidx;
+    __device__ __forceinline__ void operator=(int incl) const {
+      const unsigned long long x = w[p];
+      const unsigned long long k = x >> ib;
+      seg_id[p] = incl;
+      sidx[p] = (int32_t)(x & ((1ull << ib) - 1ull));
+      if (p == 0 || k != (w[p - 1] >> ib)) {
+        const unsigned long long m = (1ull << b) - 1ull;
+        seg_start[incl - 1] = (int32_t)p;
+        skeys[p] = (k & m) | (((k >> b) & m) << 16) | (((k >> (2 * b)) & m) << 32);
+      }
+    }
+  };
+  using reference = Ref;
+  __host__ __device__ __forceinline__ Ref operator[](int64_t i) const {
+    return Ref{w, ib, b, base + i, seg_id, seg_start, skeys, sidx};
+  }
+  __host__ __device__ __forceinline__ Ref operator*() const { return (*this)[0]; }
+  __host__ __device__ __forceinline__ SegWriter operator+(int64_t k) const {
+    SegWriter r = *this;
+    r.base += k;
+    return r;
+  }
+};
+
+__global__ void k_seg_finish(const int32_t* __restrict__ seg_id, int64_t n, int* nsegs,
+                             int32_t* seg_start, int* nsegs_mapped) {
+  const int ns = seg_id[n - 1];
+  *nsegs = ns;
+  seg_start[ns] = (int32_t)n;
+  if (nsegs_mapped) *nsegs_mapped = ns;  // host-visible (mapped pinned memory)
+}
+
 __global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n,
                                int* nsegs_mapped) {
   seg_start[*nsegs] = (int32_t)n;
@@ -108,26 +174,21 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, 
       return rc;
     k_pack_keys_idx<<<grid, 256, 0, st>>>(kin, n, lane_bits, ib, packed2);
     HRPP_LAUNCHED();
-    size_t b_sort = 0, b_sel = 0, b_scan = 0;
+    size_t b_sort = 0, b_scan = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, b_sort, packed2, sorted2, (int)n, ib,
                                    ib + 3 * lane_bits, st);
-    cub::CountingInputIterator<int32_t> cnt(0);
-    cub::DeviceSelect::Flagged(nullptr, b_sel, cnt, flags, seg->seg_start, seg->nsegs, (int)n,
-                               st);
-    cub::DeviceScan::InclusiveSum(nullptr, b_scan, flags, seg->seg_id, (int)n, st);
-    size_t b = b_sort > b_sel ? b_sort : b_sel;
-    b = b > b_scan ? b : b_scan;
+    cub::TransformInputIterator<int, HeadFlag, cub::CountingInputIterator<int64_t>> heads(
+        cub::CountingInputIterator<int64_t>(0), HeadFlag{sorted2, ib});
+    SegWriter out{sorted2, ib, lane_bits, 0, seg->seg_id, seg->seg_start, seg->skeys,
+                  seg->sidx};
+    cub::DeviceScan::InclusiveSum(nullptr, b_scan, heads, out, (int)n, st);
+    size_t b = b_sort > b_scan ? b_sort : b_scan;
     void* tmp;
     if ((rc = ws.get_raw("g_cubtmp", b, &tmp))) return rc;
     HRPP_CK(cub::DeviceRadixSort::SortKeys(tmp, b_sort, packed2, sorted2, (int)n, ib,
                                            ib + 3 * lane_bits, st));
-    k_head_flags_idx<<<grid, 256, 0, st>>>(sorted2, n, lane_bits, ib, flags, seg->skeys,
-                                           seg->sidx);
-    HRPP_LAUNCHED();
-    HRPP_CK(cub::DeviceSelect::Flagged(tmp, b_sel, cnt, flags, seg->seg_start, seg->nsegs,
-                                       (int)n, st));
-    HRPP_CK(cub::DeviceScan::InclusiveSum(tmp, b_scan, flags, seg->seg_id, (int)n, st));
-    k_seg_sentinel<<<1, 1, 0, st>>>(seg->seg_start, seg->nsegs, n, nsegs_mapped);
+    HRPP_CK(cub::DeviceScan::InclusiveSum(tmp, b_scan, heads, out, (int)n, st));
+    k_seg_finish<<<1, 1, 0, st>>>(seg->seg_id, n, seg->nsegs, seg->seg_start, nsegs_mapped);
     HRPP_LAUNCHED();
     return 0;
   }
