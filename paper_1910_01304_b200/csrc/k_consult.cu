@@ -252,7 +252,10 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
 #define HRPP_EVAL_MINB 1
 #endif
 #ifndef HRPP_FIN_MINB
-#define HRPP_FIN_MINB 1
+#define HRPP_FIN_MINB 12  // 40 registers: a fuller SM for this latency-bound walk
+#endif
+#ifndef HRPP_FIN_GRID
+#define HRPP_FIN_GRID 12  // k_finalize blocks per SM (grid-stride over rays)
 #endif
 #ifndef HRPP_REPLAY_MINB
 #define HRPP_REPLAY_MINB 6  // 80 registers (measured: consult 4.66 -> 4.11 ms on c2)
@@ -1022,7 +1025,7 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
   }
   // about one resident wave of blocks: a thread walks several rays and each
   // block flushes its tallies once
-  const int fgrid = grid_for(n, 128, num_sms() * 8);
+  const int fgrid = grid_for(n, 128, num_sms() * HRPP_FIN_GRID);
   (void)grid;
   if (closest) {
     if (live) k_finalize<true, true><<<fgrid, 128, 0, st>>>(a, n);
