@@ -1056,9 +1056,36 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   ConsultArgs a{};
   Workspace& ws = t.ws;
   if ((rc = ws.get("k_segofray", n, &a.seg_of_ray))) return rc;
-  HRPP_CK(cudaStreamSynchronize(st));
-  int nsegs_h = *(volatile int*)(pin + 32);
-  if ((rc = t.reserve(nsegs_h, n, st))) return rc;
+  // The segment count (new entries <= segments) is read back through mapped
+  // memory behind an event, and waited for only where the host needs it:
+  // after the wave-start evaluation and the fallback traversal are queued,
+  // so the GPU never idles for it.  The arena is reserved now for the
+  // wave's upper bound of appends (one per ray): a compaction moves lists,
+  // which is only safe before k_seg_lookup reads their offsets; the entry
+  // arrays and the index grow later, copy-preserving.
+  static thread_local cudaEvent_t ev_seg = nullptr;
+  if (!ev_seg) HRPP_CK(cudaEventCreateWithFlags(&ev_seg, cudaEventDisableTiming));
+  HRPP_CK(cudaEventRecord(ev_seg, st));
+  if ((rc = t.reserve(0, n, st))) return rc;
+  int nsegs_h = -1;
+  LongList LL;
+  auto resolve_nsegs = [&]() -> int {
+    if (nsegs_h >= 0) return 0;
+    HRPP_CK(cudaEventSynchronize(ev_seg));
+    nsegs_h = *(volatile int*)(pin + 32);
+    int r2;
+    if ((r2 = t.reserve(nsegs_h, n, st))) return r2;
+    a.idx = t.idx;
+    a.mask = (uint64_t)t.idx_cap - 1;
+    a.e_off = t.e_off;
+    a.e_len = t.e_len;
+    a.arena = t.arena;
+    LL.nsegs_host = nsegs_h;
+    if ((r2 = ws.get("k_lflags", nsegs_h + 1, &LL.flags)) ||
+        (r2 = ws.get("k_llist", nsegs_h + 1, &LL.list)) || (r2 = ws.get("k_lcount", 1, &LL.count)))
+      return r2;
+    return 0;
+  };
   a.nodes = b.nodes;
   a.tris = b.tris;
   a.depth = b.depth;
@@ -1086,11 +1113,6 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       (rc = ws.get("k_f1", n, &a.seg_f1)))
     return rc;
   const int grid = (int)((n + 127) / 128);
-  LongList LL;
-  LL.nsegs_host = nsegs_h;
-  if ((rc = ws.get("k_lflags", nsegs_h + 1, &LL.flags)) || (rc = ws.get("k_llist", nsegs_h + 1, &LL.list)) ||
-      (rc = ws.get("k_lcount", 1, &LL.count)))
-    return rc;
   {
     ProfScope ps(P_CONSULT, st);
     k_seg_lookup<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a, n);
@@ -1151,6 +1173,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     // rounds == 0: eval0 already marked every ray that is not a TP against the
     // wave-start entry; trace them, then one replay completes the wave.
     // rounds > 0: exact replay rounds, the last one speculative.
+    if (rounds > 0 && (rc = resolve_nsegs())) return rc;  // the replay rounds use LL
     for (int r = rounds == 0 ? rounds : 0; r <= rounds; r++) {
       if (rounds > 0) {
         a.spec = r == rounds ? 2 : 0;
@@ -1168,6 +1191,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.spec = 0;
     if (rounds == 0) {
       if ((rc = finalize_prefix(t.closest, true, grid, st, a, n, true))) return rc;
+      if ((rc = resolve_nsegs())) return rc;
       if ((rc = launch_grouped(t.closest, true, b.stack, st, a, ws, nsegs_h))) return rc;
     } else {
       if ((rc = launch_replay(t.closest, true, b.stack, st, a, ws, LL, n))) return rc;
@@ -1191,8 +1215,10 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       HRPP_LAUNCHED();
     }
     if ((rc = finalize_prefix(t.closest, false, grid, st, a, n))) return rc;
+    if ((rc = resolve_nsegs())) return rc;
     if ((rc = launch_grouped(t.closest, false, b.stack, st, a, ws, nsegs_h))) return rc;
   }
+  if ((rc = resolve_nsegs())) return rc;
   if (t.deferred)
     return table_collect_pending(t, seg, n, a.seg_napp, a.app, a.app_ray, err, st);
   // one thread per key segment (nsegs_h of them), not per ray

@@ -1,5 +1,6 @@
 # compare library variants built under exp/*/ on the bench (c2 live frame):
 # value, full traversal, ms/frame and stage times.  Usage: bash tools/exp_bench.sh [bench args]
+shopt -s nullglob
 for L in "" exp/*/libhrpp_b200.so; do
   HRPP_LIB=$L timeout 300 python bench.py --no-cpu-baseline --no-e2e "$@" > gpurun_out/eb.log 2>&1
   python - "$L" <<'PY'
