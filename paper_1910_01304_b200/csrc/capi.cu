@@ -748,8 +748,14 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
   if ((rc = ws.get("w_stats", 17, &sdev))) return rc;
   err = reinterpret_cast<int*>(sdev + 16);
   HRPP_CK(cudaMemsetAsync(sdev, 0, sizeof(unsigned long long) * 17, st));
+  // keys nobody asked for go straight into the grouping sort's packed form
+  bool prepacked = false;
   if (mode != HRPP_MODE_BASELINE) {
-    if ((rc = launch_hash(dO, dD, n, t->precision, keys, err, st))) return rc;
+    int ib = 1;  // ray index bits, as group_by_key computes them
+    while (ib < 31 && (1ll << ib) < n) ib++;
+    prepacked = out->keys == nullptr && 3 * (1 + 2 * t->precision) + ib <= 64;
+    if ((rc = launch_hash(dO, dD, n, t->precision, keys, err, st, prepacked ? ib : 0)))
+      return rc;
   }
   if (mode != HRPP_MODE_LIVE) {
     to.sums = sdev + 4;  // baseline_box_tests, baseline_tri_tests (tracer.py:361-362)
@@ -777,7 +783,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
     c.log_eval_box = lg.eval_box;
     c.log_pred_t = lg.pred_t;
     c.log_pred_slot = lg.pred_slot;
-    if ((rc = run_consult(*bvh, *t, c, keys, sdev, err, st))) return rc;
+    if ((rc = run_consult(*bvh, *t, c, keys, sdev, err, st, prepacked))) return rc;
     if ((rc = read_meta_and_finish(*t, err, st, sg, sdev))) return rc;
   } else {
     if ((rc = g_pinned.get())) return rc;

@@ -127,8 +127,9 @@ struct TableDev {
 };
 
 // ---- launchers (return HRPP status) ----
+// ib > 0: store (packed key << ib) | ray index, the grouping sort's word
 int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys, int* err,
-                cudaStream_t st);
+                cudaStream_t st, int ib = 0);
 int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err,
                        cudaStream_t st);
 // Traces n rays (or the device-counted queue ray_idx[0..*count_dev)), one
@@ -149,7 +150,7 @@ struct Segments {
 // lane_bits = 1 + 2p for hash keys (sorted on their 3(1+2p) used bits), 0 for
 // arbitrary 64-bit keys.
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, Segments* seg,
-                 cudaStream_t st, int* nsegs_mapped = nullptr);
+                 cudaStream_t st, int* nsegs_mapped = nullptr, bool prepacked = false);
 // indices i < n with flags[i] != 0, ascending, count to *count_dev
 int compact_flags(Workspace& ws, const uint8_t* flags, int64_t n, int32_t* out, int* count_dev,
                   cudaStream_t st);
@@ -185,7 +186,7 @@ struct Consult {
 // Runs the ray-ordered per-key consult of one wave and commits the table.
 // stats_dev: unsigned long long[16] device (RayKindStats order).
 int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* keys,
-                unsigned long long* stats_dev, int* err, cudaStream_t st);
+                unsigned long long* stats_dev, int* err, cudaStream_t st, bool prepacked = false);
 int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_t n,
                  uint8_t* inserted, int* err, cudaStream_t st);
 int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,

@@ -1039,7 +1039,7 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
 }
 
 int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* keys,
-                unsigned long long* stats_dev, int* err, cudaStream_t st) {
+                unsigned long long* stats_dev, int* err, cudaStream_t st, bool prepacked) {
   const int64_t n = c.n;
   if (n <= 0) return 0;
   int rc;
@@ -1051,7 +1051,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
   if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st,
-                         reinterpret_cast<int*>(pin + 32))))
+                         reinterpret_cast<int*>(pin + 32), prepacked)))
     return rc;
   ConsultArgs a{};
   Workspace& ws = t.ws;

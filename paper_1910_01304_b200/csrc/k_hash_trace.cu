@@ -30,9 +30,21 @@ __device__ __forceinline__ uint64_t ray_key(uint32_t ox, uint32_t oy, uint32_t o
          ((uint64_t)(lane_hash(oz, p) ^ lane_hash(dx, p)) << 32);
 }
 
+// The word stored for ray i: its 48-bit key (ib = 0), or, for the wave's
+// grouping sort, the three (1+2p)-bit lanes packed contiguously above the
+// ray index, (packed << ib) | i (k_pack_keys_idx's word, written here so
+// the sort needs no packing pass).
+__device__ __forceinline__ uint64_t key_word(uint64_t k, int64_t i, int p, int ib) {
+  if (ib == 0) return k;
+  const int b = 1 + 2 * p;
+  const uint64_t m = (1ull << b) - 1ull;
+  const uint64_t pk = (k & m) | (((k >> 16) & m) << b) | (((k >> 32) & m) << (2 * b));
+  return (pk << ib) | (uint64_t)i;
+}
+
 __global__ void __launch_bounds__(256) k_hash(const float* __restrict__ O,
                                               const float* __restrict__ D, int64_t n, int p,
-                                              uint64_t* __restrict__ keys, int* err) {
+                                              uint64_t* __restrict__ keys, int* err, int ib) {
   const int64_t nq = (n + 3) / 4;
   const bool vec = ((reinterpret_cast<uintptr_t>(O) | reinterpret_cast<uintptr_t>(D) |
                      reinterpret_cast<uintptr_t>(keys)) & 15) == 0;
@@ -56,10 +68,10 @@ __global__ void __launch_bounds__(256) k_hash(const float* __restrict__ O,
 #pragma unroll
       for (int k = 0; k < 12; k++) bad |= nonfinite(o[k]) | nonfinite(d[k]);
       ulonglong2 k01, k23;
-      k01.x = ray_key(o[0], o[1], o[2], d[0], d[1], d[2], p);
-      k01.y = ray_key(o[3], o[4], o[5], d[3], d[4], d[5], p);
-      k23.x = ray_key(o[6], o[7], o[8], d[6], d[7], d[8], p);
-      k23.y = ray_key(o[9], o[10], o[11], d[9], d[10], d[11], p);
+      k01.x = key_word(ray_key(o[0], o[1], o[2], d[0], d[1], d[2], p), i0, p, ib);
+      k01.y = key_word(ray_key(o[3], o[4], o[5], d[3], d[4], d[5], p), i0 + 1, p, ib);
+      k23.x = key_word(ray_key(o[6], o[7], o[8], d[6], d[7], d[8], p), i0 + 2, p, ib);
+      k23.y = key_word(ray_key(o[9], o[10], o[11], d[9], d[10], d[11], p), i0 + 3, p, ib);
       ulonglong2* kp = reinterpret_cast<ulonglong2*>(keys + i0);
       __stcs(kp, k01);
       __stcs(kp + 1, k23);
@@ -72,7 +84,7 @@ __global__ void __launch_bounds__(256) k_hash(const float* __restrict__ O,
                  d2 = __float_as_uint(D[3 * i + 2]);
         bad |= nonfinite(o0) | nonfinite(o1) | nonfinite(o2) | nonfinite(d0) | nonfinite(d1) |
                nonfinite(d2);
-        keys[i] = ray_key(o0, o1, o2, d0, d1, d2, p);
+        keys[i] = key_word(ray_key(o0, o1, o2, d0, d1, d2, p), i, p, ib);
       }
     }
   }
@@ -132,7 +144,8 @@ __device__ __forceinline__ uint32_t tile_bytes(int64_t t, int64_t n) {
 
 __global__ void __launch_bounds__(256) k_hash_bulk(const float* __restrict__ O,
                                                    const float* __restrict__ D, int64_t n,
-                                                   int p, uint64_t* __restrict__ keys, int* err) {
+                                                   int p, uint64_t* __restrict__ keys, int* err,
+                                                   int ib) {
   const int64_t ntiles = (n + kHashTile - 1) / kHashTile;
   extern __shared__ __align__(128) unsigned char hsm[];
   float* so = reinterpret_cast<float*>(hsm);                                  // [stages][3072]
@@ -170,7 +183,7 @@ __global__ void __launch_bounds__(256) k_hash_bulk(const float* __restrict__ O,
                        d2 = __float_as_uint(D[3 * i + 2]);
         bad |= nonfinite(o0) | nonfinite(o1) | nonfinite(o2) | nonfinite(d0) | nonfinite(d1) |
                nonfinite(d2);
-        keys[i] = ray_key(o0, o1, o2, d0, d1, d2, p);
+        keys[i] = key_word(ray_key(o0, o1, o2, d0, d1, d2, p), i, p, ib);
       }
     } else {
     const float4* o4 = reinterpret_cast<const float4*>(so + sI * (kHashTile * 3) + 12 * tid);
@@ -188,10 +201,10 @@ __global__ void __launch_bounds__(256) k_hash_bulk(const float* __restrict__ O,
 #pragma unroll
     for (int j = 0; j < 12; j++) bad |= nonfinite(o[j]) | nonfinite(d[j]);
     ulonglong2 k01, k23;
-    k01.x = ray_key(o[0], o[1], o[2], d[0], d[1], d[2], p);
-    k01.y = ray_key(o[3], o[4], o[5], d[3], d[4], d[5], p);
-    k23.x = ray_key(o[6], o[7], o[8], d[6], d[7], d[8], p);
-    k23.y = ray_key(o[9], o[10], o[11], d[9], d[10], d[11], p);
+    k01.x = key_word(ray_key(o[0], o[1], o[2], d[0], d[1], d[2], p), i0, p, ib);
+    k01.y = key_word(ray_key(o[3], o[4], o[5], d[3], d[4], d[5], p), i0 + 1, p, ib);
+    k23.x = key_word(ray_key(o[6], o[7], o[8], d[6], d[7], d[8], p), i0 + 2, p, ib);
+    k23.y = key_word(ray_key(o[9], o[10], o[11], d[9], d[10], d[11], p), i0 + 3, p, ib);
     ulonglong2* kp = reinterpret_cast<ulonglong2*>(keys + i0);
     __stcs(kp, k01);
     __stcs(kp + 1, k23);
@@ -208,7 +221,7 @@ __global__ void __launch_bounds__(256) k_hash_bulk(const float* __restrict__ O,
 }
 
 int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys, int* err,
-                cudaStream_t st) {
+                cudaStream_t st, int ib) {
   if (n <= 0) return 0;
   ProfScope ps(P_HASH, st);
   const bool aligned = ((reinterpret_cast<uintptr_t>(O) | reinterpret_cast<uintptr_t>(D) |
@@ -221,9 +234,9 @@ int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys
       HRPP_CK(cudaFuncSetAttribute(k_hash_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       smem_set = 1;
     }
-    k_hash_bulk<<<2 * num_sms(), 256, smem, st>>>(O, D, n, p, keys, err);
+    k_hash_bulk<<<2 * num_sms(), 256, smem, st>>>(O, D, n, p, keys, err, ib);
   } else {  // small or unaligned batches
-    k_hash<<<grid_for((n + 3) / 4, 256, num_sms() * 8), 256, 0, st>>>(O, D, n, p, keys, err);
+    k_hash<<<grid_for((n + 3) / 4, 256, num_sms() * 8), 256, 0, st>>>(O, D, n, p, keys, err, ib);
   }
   HRPP_LAUNCHED();
   return 0;

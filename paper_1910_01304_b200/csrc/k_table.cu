@@ -150,7 +150,7 @@ __global__ void k_seg_sentinel(int32_t* seg_start, const int* nsegs, int64_t n,
 }
 
 int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, Segments* seg,
-                 cudaStream_t st, int* nsegs_mapped) {
+                 cudaStream_t st, int* nsegs_mapped, bool prepacked) {
   int32_t* iota;
   int32_t* flags;
   unsigned long long* packed = nullptr;
@@ -172,8 +172,12 @@ int group_by_key(Workspace& ws, const uint64_t* keys, int64_t n, int lane_bits, 
     unsigned long long *packed2, *sorted2;
     if ((rc = ws.get("g_packed", n, &packed2)) || (rc = ws.get("g_psorted", n, &sorted2)))
       return rc;
-    k_pack_keys_idx<<<grid, 256, 0, st>>>(kin, n, lane_bits, ib, packed2);
-    HRPP_LAUNCHED();
+    if (prepacked) {  // the hash kernel already wrote (packed << ib) | i
+      packed2 = const_cast<unsigned long long*>(kin);
+    } else {
+      k_pack_keys_idx<<<grid, 256, 0, st>>>(kin, n, lane_bits, ib, packed2);
+      HRPP_LAUNCHED();
+    }
     size_t b_sort = 0, b_scan = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, b_sort, packed2, sorted2, (int)n, ib,
                                    ib + 3 * lane_bits, st);
