@@ -547,14 +547,25 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_long(ConsultAr
 // with at most G rays left (the rays after its first append), 32/G segments
 // per warp.  Within a group this is seg_warp's ballot loop.
 template <bool CLOSEST, bool LIVE, int STACK, int G>
-__global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultArgs a, const int32_t* list,
-                                                      int count) {
+__global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultArgs a, const int32_t* ids,
+                                                      const int* bounds, int K, int* ticket) {
   if (*a.err) return;
+  // Persistent blocks take 128 / G segments at a time from the class's
+  // ticket; the class (list, count) is read on the device, so the host
+  // launches without waiting for the class bounds.
+  const int32_t* list = ids + bounds[K];
+  const int count = bounds[K + 1] - bounds[K];
   const int lane = threadIdx.x & 31;
   const int gl = lane % G, gbase = lane - gl;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
-  const int gid = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
   Tally c;
+  __shared__ int s_base;
+  for (;;) {
+  __syncthreads();  // s_base of the previous batch read by every thread
+  if (threadIdx.x == 0) s_base = atomicAdd(ticket, 128 / G);
+  __syncthreads();
+  if (s_base >= count) break;
+  const int gid = s_base + (int)threadIdx.x / G;
   const bool gvalid = gid < count;
   int s = 0;
   int32_t beg = 0, end = 0, tb = 0, napp = 0, ex_len = 0;
@@ -628,6 +639,7 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultA
     a.seg_napp[s] = napp;
     a.seg_cursor[s] = end;
   }
+  }
   flush_tally_warp(c, a.stats);
 }
 
@@ -648,13 +660,26 @@ constexpr int kBlockReplayMin = 1024;
 
 template <bool CLOSEST, bool LIVE, int STACK, int BS>
 __global__ void __launch_bounds__(BS, BS == 32 ? HRPP_BLOCK32_MINB : HRPP_BLOCK_MINB)
-    k_replay_block(ConsultArgs a, const int32_t* list, int count) {
+    k_replay_block(ConsultArgs a, const int32_t* list, int count, const int* bounds, int K,
+                   int* ticket) {
   if (*a.err) return;
   __shared__ int s_f;
   __shared__ int32_t s_cf, s_rf;
+  __shared__ int s_k;
   const int tid = threadIdx.x;
+  if (bounds) {  // class read on the device; persistent blocks take tickets
+    list += bounds[K];
+    count = bounds[K + 1] - bounds[K];
+  }
   Tally c;
-  for (int k = blockIdx.x; k < count; k += gridDim.x) {
+  for (int k = blockIdx.x;;) {
+    if (bounds) {
+      __syncthreads();
+      if (tid == 0) s_k = atomicAdd(ticket, 1);
+      __syncthreads();
+      k = s_k;
+    }
+    if (k >= count) break;
     const int s = list[k];
     const int32_t beg = a.seg_start[s], end = a.seg_start[s + 1];
     int32_t tb = a.seg_cursor[s];
@@ -724,6 +749,7 @@ __global__ void __launch_bounds__(BS, BS == 32 ? HRPP_BLOCK32_MINB : HRPP_BLOCK_
       a.seg_napp[s] = napp;
       a.seg_cursor[s] = end;
     }
+    if (!bounds) k += gridDim.x;
   }
   flush_tally(c, a.stats);
 }
@@ -769,7 +795,8 @@ __global__ void k_replay_class(ConsultArgs a, int64_t nseg_cap, uint8_t* cls, in
 }
 
 // Start of every class in the class-sorted list (9 entries + end).
-__global__ void k_class_bounds(const uint8_t* sorted_cls, int64_t m, int* bounds) {
+__global__ void k_class_bounds(const uint8_t* sorted_cls, int64_t m, int* bounds,
+                               int* bounds_mapped) {
   const int k = threadIdx.x;
   if (k > 9) return;
   int64_t lo = 0, hi = m;  // first position with class >= k
@@ -779,6 +806,7 @@ __global__ void k_class_bounds(const uint8_t* sorted_cls, int64_t m, int* bounds
     else hi = mid;
   }
   bounds[k] = (int)lo;
+  if (bounds_mapped) bounds_mapped[k] = (int)lo;
 }
 
 // Flags of the active segments longer than short_len.
@@ -903,12 +931,18 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   int hb[10];
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
-  // bounds written straight into this thread's mapped pinned buffer
-  k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, reinterpret_cast<int*>(pin + 40));
+  int *bounds, *tickets;
+  if ((rc = ws.get("rg_bounds", 10, &bounds)) || (rc = ws.get("rg_tickets", 10, &tickets)))
+    return rc;
+  HRPP_CK(cudaMemsetAsync(tickets, 0, sizeof(int) * 10, st));
+  // class bounds to the device (read there by the class kernels) and to this
+  // thread's mapped pinned buffer (the host needs only class 8's count,
+  // waited for behind an event once classes 1-7 are queued)
+  k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds, reinterpret_cast<int*>(pin + 40));
   HRPP_LAUNCHED();
-  HRPP_CK(cudaStreamSynchronize(st));
-  memcpy(hb, (const void*)(pin + 40), sizeof(int) * 10);
-  auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
+  static thread_local cudaEvent_t ev_cls = nullptr;
+  if (!ev_cls) HRPP_CK(cudaEventCreateWithFlags(&ev_cls, cudaEventDisableTiming));
+  HRPP_CK(cudaEventRecord(ev_cls, st));
   // The classes hold disjoint segments, so their kernels run concurrently:
   // each is small and latency-bound (a few hundred blocks, or one long
   // chain per segment), and back to back each one's tail idled the GPU.
@@ -922,13 +956,17 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
     used |= 1 << (k % HRPP_REPLAY_STREAMS);
     return s2;
   };
-#define HRPP_GROUP(K, GS)                                                                      \
-  if (cnt(K) > 0) {                                                                            \
-    const int64_t thr = (int64_t)cnt(K) * GS;                                                  \
-    k_replay_group<CLOSEST, LIVE, STACK, GS><<<(int)((thr + 127) / 128), 128, 0, side(K)>>>(  \
-        a, ids_sorted + hb[K], cnt(K));                                                        \
-    HRPP_LAUNCHED();                                                                           \
-  }
+  // persistent grids: at most one resident wave of blocks, at most what the
+  // segment count could need
+  auto pgrid = [&](int64_t per_block, int64_t resident) -> int {
+    const int64_t need = (m + per_block - 1) / per_block;
+    const int64_t cap = (int64_t)num_sms() * resident;
+    return (int)(need < cap ? (need > 0 ? need : 1) : cap);
+  };
+#define HRPP_GROUP(K, GS)                                                                     \
+  k_replay_group<CLOSEST, LIVE, STACK, GS><<<pgrid(128 / GS, 6), 128, 0, side(K)>>>(         \
+      a, ids_sorted, bounds, K, tickets + K);                                                 \
+  HRPP_LAUNCHED();
   HRPP_GROUP(1, 1)
   HRPP_GROUP(2, 2)
   HRPP_GROUP(3, 4)
@@ -936,11 +974,13 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   HRPP_GROUP(5, 16)
   HRPP_GROUP(6, 32)
 #undef HRPP_GROUP
-  if (cnt(7) > 0) {  // long segments: a warp each, 32-ray tiles
-    k_replay_block<CLOSEST, LIVE, STACK, 32><<<cnt(7), 32, 0, side(7)>>>(a, ids_sorted + hb[7],
-                                                                           cnt(7));
-    HRPP_LAUNCHED();
-  }
+  // long segments: a warp each, 32-ray tiles
+  k_replay_block<CLOSEST, LIVE, STACK, 32><<<pgrid(1, HRPP_BLOCK32_MINB), 32, 0, side(7)>>>(
+      a, ids_sorted, 0, bounds, 7, tickets + 7);
+  HRPP_LAUNCHED();
+  HRPP_CK(cudaEventSynchronize(ev_cls));
+  memcpy(hb, (const void*)(pin + 40), sizeof(int) * 10);
+  auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
   // class 8 below runs on st after the join (it sorts by remaining length)
   for (int k = 0; k < HRPP_REPLAY_STREAMS; k++)
     if (used & (1 << k)) {
@@ -963,7 +1003,8 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
     if ((rc = ws.get_raw("rg_tmp8", b8, &tmp8))) return rc;
     HRPP_CK(cub::DeviceRadixSort::SortPairsDescending(tmp8, b8, rem, rem2, ids_sorted + hb[8],
                                                       ids8, c8, 0, 32, st));
-    k_replay_block<CLOSEST, LIVE, STACK, kBlockReplay><<<c8, kBlockReplay, 0, st>>>(a, ids8, c8);
+    k_replay_block<CLOSEST, LIVE, STACK, kBlockReplay><<<c8, kBlockReplay, 0, st>>>(
+        a, ids8, c8, nullptr, 0, nullptr);
     HRPP_LAUNCHED();
   }
   return 0;
