@@ -892,6 +892,7 @@ static int launch_replay(bool closest, bool live, int stack, cudaStream_t st,
 struct SidePool {
   cudaStream_t s[8];
   cudaEvent_t fork, join[8];
+  cudaEvent_t seg_ready, cls_ready;  // segment count / class bounds written
 };
 
 static SidePool& side_pool() {
@@ -906,6 +907,8 @@ static SidePool& side_pool() {
       cudaEventCreateWithFlags(&p.join[k], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p.seg_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p.cls_ready, cudaEventDisableTiming);
     it = pools.emplace(dev, p).first;
   }
   return it->second;
@@ -940,8 +943,7 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   // waited for behind an event once classes 1-7 are queued)
   k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds, reinterpret_cast<int*>(pin + 40));
   HRPP_LAUNCHED();
-  static thread_local cudaEvent_t ev_cls = nullptr;
-  if (!ev_cls) HRPP_CK(cudaEventCreateWithFlags(&ev_cls, cudaEventDisableTiming));
+  const cudaEvent_t ev_cls = side_pool().cls_ready;
   HRPP_CK(cudaEventRecord(ev_cls, st));
   // The classes hold disjoint segments, so their kernels run concurrently:
   // each is small and latency-bound (a few hundred blocks, or one long
@@ -1104,8 +1106,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   // wave's upper bound of appends (one per ray): a compaction moves lists,
   // which is only safe before k_seg_lookup reads their offsets; the entry
   // arrays and the index grow later, copy-preserving.
-  static thread_local cudaEvent_t ev_seg = nullptr;
-  if (!ev_seg) HRPP_CK(cudaEventCreateWithFlags(&ev_seg, cudaEventDisableTiming));
+  const cudaEvent_t ev_seg = side_pool().seg_ready;  // per host thread and device
   HRPP_CK(cudaEventRecord(ev_seg, st));
   if ((rc = t.reserve(0, n, st))) return rc;
   int nsegs_h = -1;
