@@ -264,11 +264,20 @@ def run_ours(args, rank, world, local_rank):
             merge_wave_records(table, dist, ray_offset=offsets[j])
         return out
 
+    # output buffers reused frame to frame (trace_wave(outputs=...)), as a
+    # renderer would; live mode writes found/t/slot/leaf
+    wave_out = [{"found": torch.empty(w[1].shape[0], dtype=torch.bool, device=dev),
+                 "t": torch.empty(w[1].shape[0], dtype=torch.float64, device=dev),
+                 "slot": torch.empty(w[1].shape[0], dtype=torch.int32, device=dev),
+                 "leaf": torch.empty(w[1].shape[0], dtype=torch.int32, device=dev)}
+                for w in dwaves]
+
     def frame(mode, stats=None):
         for t in tables.values():
-            t.clear()
+            t.clear()  # stream-ordered (hrpp_table_clear_async)
         for j, (closest, O, D, t0, t1) in enumerate(dwaves):
-            run_wave(j, mode, O, D, t0, t1, stats=stats[waves[j][1]] if stats is not None else None)
+            run_wave(j, mode, O, D, t0, t1, stats=stats[waves[j][1]] if stats is not None else None,
+                     outputs=wave_out[j] if mode == "live" and not keyed else None)
 
     def barrier():
         if multi:

@@ -154,6 +154,8 @@ int hrpp_table_create(int precision, int go_up_level, int kind, int64_t max_entr
                       int device, hrpp_table_t *out);
 int hrpp_table_destroy(hrpp_table_t table);
 int hrpp_table_clear(hrpp_table_t table);
+/* the same, stream-ordered on `stream` (host returns at once) */
+int hrpp_table_clear_async(hrpp_table_t table, void *stream);
 /* entries, stored nodes, max nodes per entry (predictor.py:135-141). */
 int hrpp_table_info(hrpp_table_t table, int64_t *entries, int64_t *stored, int64_t *max_len);
 /* predictor.py:147-160 record, batched with sequential semantics (ray order):

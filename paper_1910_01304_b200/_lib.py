@@ -67,6 +67,7 @@ def _load():
     L.hrpp_table_create.argtypes = [C.c_int, C.c_int, C.c_int, I64, C.c_int, P]
     L.hrpp_table_destroy.argtypes = [P]
     L.hrpp_table_clear.argtypes = [P]
+    L.hrpp_table_clear_async.argtypes = [P, P]
     L.hrpp_table_info.argtypes = [P, P, P, P]
     L.hrpp_table_record.argtypes = [P, P, P, I64, P, P]
     L.hrpp_table_lookup.argtypes = [P, C.c_uint64, P, I64, P]
@@ -85,7 +86,7 @@ def _load():
                  "hrpp_hash_floats", "hrpp_bvh_create", "hrpp_bvh_destroy",
                  "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch",
                  "hrpp_table_create", "hrpp_table_destroy", "hrpp_table_clear",
-                 "hrpp_table_info", "hrpp_table_record", "hrpp_table_lookup",
+                 "hrpp_table_clear_async", "hrpp_table_info", "hrpp_table_record", "hrpp_table_lookup",
                  "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
                  "hrpp_profile_enable", "hrpp_profile_read", "hrpp_table_set_deferred",
                  "hrpp_table_pending", "hrpp_set_consult_short",
@@ -114,7 +115,8 @@ lib = _LazyLib()
 EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device_count",
             "hrpp_hash_rays", "hrpp_hash_floats", "hrpp_bvh_create", "hrpp_bvh_destroy",
             "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch", "hrpp_table_create",
-            "hrpp_table_destroy", "hrpp_table_clear", "hrpp_table_info", "hrpp_table_record",
+            "hrpp_table_destroy", "hrpp_table_clear", "hrpp_table_clear_async", "hrpp_table_info",
+            "hrpp_table_record",
             "hrpp_table_lookup", "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
             "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
             "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short",
@@ -216,6 +218,19 @@ def stream_of(like):
     if like is not None and is_torch(like) and like.is_cuda:
         import torch
         return C.c_void_p(torch.cuda.current_stream(like.device).cuda_stream)
+    return None
+
+
+def current_stream_handle(device=None):
+    """torch's current CUDA stream (raw handle) if torch with CUDA is in use,
+    else None (the legacy default stream)."""
+    import sys
+    torch = sys.modules.get("torch")
+    try:
+        if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+            return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    except Exception:
+        pass
     return None
 
 

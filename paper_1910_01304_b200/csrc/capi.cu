@@ -550,12 +550,20 @@ int hrpp_table_destroy(hrpp_table_t table) {
   return HRPP_OK;
 }
 
-int hrpp_table_clear(hrpp_table_t t) {
+int hrpp_table_clear_async(hrpp_table_t t, void* stream) {
   CHECK_ARG(t, "null table");
   HRPP_CK(cudaSetDevice(t->device));
-  HRPP_CK(cudaMemset(t->meta, 0, sizeof(long long) * 4));
-  if (t->idx) HRPP_CK(cudaMemset(t->idx, 0xFF, sizeof(Bucket) * t->idx_cap));
-  t->n_entries = t->stored = t->arena_used = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (t->meta) HRPP_CK(cudaMemsetAsync(t->meta, 0, sizeof(long long) * 4, st));
+  if (t->idx) HRPP_CK(cudaMemsetAsync(t->idx, 0xFF, sizeof(Bucket) * t->idx_cap, st));
+  t->n_entries = t->stored = t->arena_used = t->pending = 0;
+  return HRPP_OK;
+}
+
+int hrpp_table_clear(hrpp_table_t t) {
+  int rc = hrpp_table_clear_async(t, nullptr);
+  if (rc) return rc;
+  HRPP_CK(cudaStreamSynchronize(nullptr));
   return HRPP_OK;
 }
 

@@ -235,9 +235,14 @@ class PredictorTable:
                                                    _lib.ptr(rays), m, C.byref(cnt)), "pending")
         return keys, nodes, rays
 
-    def clear(self):
+    def clear(self, stream=None):
+        """Empty the table (capacity kept).  Stream-ordered on ``stream`` (a
+        torch stream or raw handle; default: torch's current stream when a
+        device is in use), so the host does not wait."""
         if self._handle is not None:
-            _lib.check(_lib.lib.hrpp_table_clear(self._handle), "clear")
+            st = (_lib.current_stream_handle(self._device) if stream is None
+                  else C.c_void_p(getattr(stream, "cuda_stream", stream)))
+            _lib.check(_lib.lib.hrpp_table_clear_async(self._handle, st), "clear")
 
     # -- prediction (predictor.py:167-197) ---------------------------------------------
 
