@@ -196,8 +196,15 @@ def as_array(a, dtype, like=None, shape=None):
     """Contiguous array of `dtype`, on the device if `a` is a CUDA tensor."""
     if is_torch(a):
         import torch
-        t = a.to(dtype=getattr(torch, _TORCH_DT[dtype])).contiguous()
-        return t.reshape(shape) if shape is not None else t
+        tdt = getattr(torch, _TORCH_DT[dtype])
+        t = a if a.dtype == tdt else a.to(dtype=tdt)
+        if not t.is_contiguous():
+            t = t.contiguous()
+        if shape is None:
+            return t
+        if len(shape) == 2 and t.dim() == 2 and t.shape[1] == shape[1]:
+            return t  # already (n, k): no view object per call (wave hot path)
+        return t.reshape(shape)
     out = np.ascontiguousarray(a, dtype=dtype)
     return out.reshape(shape) if shape is not None else out
 
