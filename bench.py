@@ -534,6 +534,9 @@ def run_ours(args, rank, world, local_rank):
             "live_stats": {k: dict(zip(STATS_NAMES, map(int, live_stats[k]))) for k in kinds},
             "stages": stages,
             "stages_note": "per-stage CUDA events in a separate untimed pass of the same frames; "
+                           "a live wave on an empty table (the first wave of each ray kind) "
+                           "traces on a side stream concurrently with its grouping, so "
+                           "group and trace_queue overlap and the stages sum past the frame; "
                            "the roofline stage alone is event-timed inside the timed region",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk.summary(),

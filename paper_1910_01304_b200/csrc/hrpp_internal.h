@@ -137,7 +137,8 @@ int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err
 int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const double* tmin, const double* tmax, int32_t start, int64_t n,
                  const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
-                 const int* err, cudaStream_t st, Workspace* ws = nullptr);
+                 const int* err, cudaStream_t st, Workspace* ws = nullptr,
+                 bool fallback = false);  // fallback: profiled as the live fallback traversal
 
 // Group a batch of keys: stable sort (key, ray) and find key segments.
 struct Segments {

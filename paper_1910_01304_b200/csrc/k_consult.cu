@@ -33,6 +33,10 @@
 
 namespace hrpp {
 
+#ifndef HRPP_EARLY_TRACE
+#define HRPP_EARLY_TRACE 1
+#endif
+
 int g_live_rounds = 0;
 int g_consult_short = 32;  // segments up to this many rays are replayed by one lane
 
@@ -893,6 +897,7 @@ struct SidePool {
   cudaStream_t s[8];
   cudaEvent_t fork, join[8];
   cudaEvent_t seg_ready, cls_ready;  // segment count / class bounds written
+  cudaEvent_t trace_done;            // early fallback traversal finished
 };
 
 static SidePool& side_pool() {
@@ -909,6 +914,7 @@ static SidePool& side_pool() {
     cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&p.seg_ready, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&p.cls_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p.trace_done, cudaEventDisableTiming);
     it = pools.emplace(dev, p).first;
   }
   return it->second;
@@ -1093,6 +1099,37 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   // index stays sized to the table (L2-resident for c1-c3 tables), not to the wave
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
+  // A live wave on an empty table needs every ray's full traversal (no
+  // entry can make a ray a TP before its segment's first append), and that
+  // traversal needs nothing from the grouping: it starts at once on a side
+  // stream, overlapped with the sort and segment construction (memory-bound
+  // against the issue-bound traversal), and joins before the first-append
+  // bids and the replay.  The first wave of each ray kind in a frame.
+  const int rounds0 = g_live_rounds < 0 ? 0 : g_live_rounds;
+  const bool early_trace = c.live && rounds0 == 0 && t.n_entries == 0 && HRPP_EARLY_TRACE;
+  if (early_trace) {
+    uint8_t* f_known;
+    int32_t *f_box, *f_tri;
+    if ((rc = t.ws.get("v_fknown", n, &f_known)) || (rc = t.ws.get("v_fbox32", n, &f_box)) ||
+        (rc = t.ws.get("v_ftri32", n, &f_tri)))
+      return rc;
+    SidePool& sp = side_pool();
+    HRPP_CK(cudaEventRecord(sp.fork, st));
+    HRPP_CK(cudaStreamWaitEvent(sp.s[0], sp.fork, 0));
+    TraceOut to;
+    to.found = c.o_found;
+    to.t = c.o_t;
+    to.slot = c.o_slot;
+    to.leaf = c.o_leaf;
+    to.box32 = f_box;
+    to.tri32 = f_tri;
+    to.known = f_known;  // every ray: known = 1
+    to.zero_miss_t = true;
+    if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, nullptr, nullptr, to,
+                           err, sp.s[0], &t.ws, true)))
+      return rc;
+    HRPP_CK(cudaEventRecord(sp.trace_done, sp.s[0]));
+  }
   if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st,
                          reinterpret_cast<int*>(pin + 32), prepacked)))
     return rc;
@@ -1187,8 +1224,10 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.o_leaf = c.o_leaf;
     // coalesced presets instead of two scattered byte stores per ray in eval0
     a.f_known_clear = nullptr;
-    HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
-    HRPP_CK(cudaMemsetAsync(a.need, rounds > 0 ? 0 : 1, n, st));  // eval0 clears the TPs
+    if (!early_trace) {  // (the early traversal writes known = 1 for every ray)
+      HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
+      HRPP_CK(cudaMemsetAsync(a.need, rounds > 0 ? 0 : 1, n, st));  // eval0 clears the TPs
+    }
     {
       ProfScope ps(P_CONSULT, st);
       if (t.closest) dispatch_eval0<true>(b.stack, grid, st, a, n, rounds == 0, t.n_entries == 0);
@@ -1216,7 +1255,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     // wave-start entry; trace them, then one replay completes the wave.
     // rounds > 0: exact replay rounds, the last one speculative.
     if (rounds > 0 && (rc = resolve_nsegs())) return rc;  // the replay rounds use LL
-    for (int r = rounds == 0 ? rounds : 0; r <= rounds; r++) {
+    for (int r = rounds == 0 ? rounds : 0; r <= rounds && !early_trace; r++) {
       if (rounds > 0) {
         a.spec = r == rounds ? 2 : 0;
         HRPP_CK(cudaMemsetAsync(a.need, 0, n, st));
@@ -1231,7 +1270,12 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
         return rc;
     }
     a.spec = 0;
-    if (rounds == 0) {
+    if (early_trace) {  // join the early traversal; the first-append bids run here
+      HRPP_CK(cudaStreamWaitEvent(st, side_pool().trace_done, 0));
+      if ((rc = resolve_nsegs())) return rc;
+      if ((rc = finalize_prefix(t.closest, true, grid, st, a, n, false))) return rc;
+      if ((rc = launch_grouped(t.closest, true, b.stack, st, a, ws, nsegs_h))) return rc;
+    } else if (rounds == 0) {
       if ((rc = finalize_prefix(t.closest, true, grid, st, a, n, true))) return rc;
       if ((rc = resolve_nsegs())) return rc;
       if ((rc = launch_grouped(t.closest, true, b.stack, st, a, ws, nsegs_h))) return rc;

@@ -364,11 +364,11 @@ static void dispatch_trace(int stack, int grid, cudaStream_t st, const TraceArgs
 int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
                  const double* tmin, const double* tmax, int32_t start, int64_t n,
                  const int32_t* ray_idx, const int* count_dev, const TraceOut& out,
-                 const int* err, cudaStream_t st, Workspace* ws) {
+                 const int* err, cudaStream_t st, Workspace* ws, bool fallback) {
   (void)ws;
   if (n <= 0) return 0;
   TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
-  ProfScope ps(ray_idx ? P_TRACE_QUEUE : P_TRACE, st);
+  ProfScope ps(ray_idx || fallback ? P_TRACE_QUEUE : P_TRACE, st);
   const int grid = (int)((n + 127) / 128);
   if (closest) dispatch_trace<true>(b.stack, grid, st, a);
   else dispatch_trace<false>(b.stack, grid, st, a);

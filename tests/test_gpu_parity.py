@@ -795,3 +795,36 @@ def test_exchange_rows_round_trip(hb):
         ref = torch.empty_like(hits[k])
         ref[p] = hits[k]
         assert torch.equal(out[k], ref), k
+
+def test_table_clear_reuse_equals_fresh(hb):
+    """A cleared table (stream-ordered clear, capacity kept) behaves exactly
+    like a fresh one: same hits, statistics and dump over a wave sequence."""
+    import torch
+    from paper_1910_01304_b200 import scenes
+    sc = scenes.make_scene("c1", resolution=(96, 96))
+    b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
+    O, D = scenes.primary_rays(sc.camera, 2, seed=4)
+    n = O.shape[0]
+    dev = torch.device("cuda")
+    Ot, Dt = torch.from_numpy(O).to(dev), torch.from_numpy(D).to(dev)
+    t0 = torch.zeros(n, dtype=torch.float64, device=dev)
+    t1 = torch.full((n,), float("inf"), dtype=torch.float64, device=dev)
+
+    def run(table):
+        res = []
+        for mode in ("live", "limit"):
+            out, st = hb.trace_wave(b, table, mode, Ot, Dt, t0, t1, True)
+            res.append(({k: v.cpu().numpy() for k, v in out.items()}, st.copy(),
+                        list(table.dump_lines())))
+        return res
+
+    used = hb.PredictorTable(hb.HashConfig(5), 1, hb.RayKind.CLOSEST_HIT)
+    run(used)
+    used.clear()
+    got = run(used)
+    ref = run(hb.PredictorTable(hb.HashConfig(5), 1, hb.RayKind.CLOSEST_HIT))
+    for (go, gs, gd), (ro, rs, rd) in zip(got, ref):
+        assert np.array_equal(gs, rs)
+        assert gd == rd
+        for k in ro:
+            assert np.array_equal(go[k], ro[k]), k
