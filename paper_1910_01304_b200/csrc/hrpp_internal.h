@@ -120,6 +120,7 @@ struct TableDev {
   // (key, node, ray index) wait in ws "p_keys"/"p_nodes"/"p_rays", sorted by ray
   bool deferred = false;
   int64_t pending = 0;
+  double start_tp_frac = 1.0;  // wave-start TP fraction of the last live wave
   Workspace ws;
   ~TableDev();
   // capacity for up to extra_entries new entries and extra_nodes new nodes

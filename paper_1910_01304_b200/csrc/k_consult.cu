@@ -41,6 +41,7 @@ int g_live_rounds = 0;
 int g_consult_short = 32;  // segments up to this many rays are replayed by one lane
 
 enum { S_RAYS, S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG };
+constexpr int S_START_TP = 14;  // (library-internal) TPs against the wave-start table
 
 // Running eval_entry result of one ray (by ray index): 32 bytes, two 16-B
 // accesses.  `applied` = number of entry nodes already folded.
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(128, HRPP_FIN_MINB) k_finalize(ConsultArgs a, 
 template <bool CLOSEST, int STACK>
 __global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
   if (*a.err) return;
+  unsigned long long tps = 0;  // wave-start TPs (the early-traversal policy)
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int32_t i = a.sidx[p];
@@ -358,7 +360,10 @@ __global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, in
     // need[] is preset to 1 (coalesced memset): only the wave-start TPs,
     // rare, are cleared here with a scattered store
     if (mark_need && ex_len > 0 && acc.found) a.need[i] = 0;
+    tps += ex_len > 0 && acc.found;
   }
+  tps = warp_sum(tps);
+  if ((threadIdx.x & 31) == 0 && tps) atomicAdd(a.stats + S_START_TP, tps);
 }
 
 // ---------------------------------------------------------------------------
@@ -1106,7 +1111,14 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   // against the issue-bound traversal), and joins before the first-append
   // bids and the replay.  The first wave of each ray kind in a frame.
   const int rounds0 = g_live_rounds < 0 ? 0 : g_live_rounds;
-  const bool early_trace = c.live && rounds0 == 0 && t.n_entries == 0 && HRPP_EARLY_TRACE;
+  // Also when the table is not empty but its last live wave had few
+  // wave-start TPs (under 5 %): the early traversal then also traces those
+  // few TPs (their outputs are overwritten by the entry result), a small
+  // waste against the overlap won.
+  const bool early_trace =
+      c.live && rounds0 == 0 &&
+      (HRPP_EARLY_TRACE == 2 ||
+       (HRPP_EARLY_TRACE == 1 && (t.n_entries == 0 || t.start_tp_frac < 0.05)));
   if (early_trace) {
     uint8_t* f_known;
     int32_t *f_box, *f_tri;
