@@ -557,13 +557,14 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_long(ConsultAr
 // per warp.  Within a group this is seg_warp's ballot loop.
 template <bool CLOSEST, bool LIVE, int STACK, int G>
 __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultArgs a, const int32_t* ids,
-                                                      const int* bounds, int K, int* ticket) {
+                                                      const int* counts, int64_t cap, int K,
+                                                      int* ticket) {
   if (*a.err) return;
   // Persistent blocks take 128 / G segments at a time from the class's
   // ticket; the class (list, count) is read on the device, so the host
   // launches without waiting for the class bounds.
-  const int32_t* list = ids + bounds[K];
-  const int count = bounds[K + 1] - bounds[K];
+  const int32_t* list = ids + (int64_t)K * cap;
+  const int count = counts[K];
   const int lane = threadIdx.x & 31;
   const int gl = lane % G, gbase = lane - gl;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
@@ -669,20 +670,20 @@ constexpr int kBlockReplayMin = 1024;
 
 template <bool CLOSEST, bool LIVE, int STACK, int BS>
 __global__ void __launch_bounds__(BS, BS == 32 ? HRPP_BLOCK32_MINB : HRPP_BLOCK_MINB)
-    k_replay_block(ConsultArgs a, const int32_t* list, int count, const int* bounds, int K,
-                   int* ticket) {
+    k_replay_block(ConsultArgs a, const int32_t* list, int count, const int* counts,
+                   int64_t cap, int K, int* ticket) {
   if (*a.err) return;
   __shared__ int s_f;
   __shared__ int32_t s_cf, s_rf;
   __shared__ int s_k;
   const int tid = threadIdx.x;
-  if (bounds) {  // class read on the device; persistent blocks take tickets
-    list += bounds[K];
-    count = bounds[K + 1] - bounds[K];
+  if (counts) {  // class read on the device; persistent blocks take tickets
+    list += (int64_t)K * cap;
+    count = counts[K];
   }
   Tally c;
   for (int k = blockIdx.x;;) {
-    if (bounds) {
+    if (counts) {
       __syncthreads();
       if (tid == 0) s_k = atomicAdd(ticket, 1);
       __syncthreads();
@@ -758,7 +759,7 @@ __global__ void __launch_bounds__(BS, BS == 32 ? HRPP_BLOCK32_MINB : HRPP_BLOCK_
       a.seg_napp[s] = napp;
       a.seg_cursor[s] = end;
     }
-    if (!bounds) k += gridDim.x;
+    if (!counts) k += gridDim.x;
   }
   flush_tally(c, a.stats);
 }
@@ -771,52 +772,52 @@ __global__ void k_seg_remaining(ConsultArgs a, const int32_t* list, int m, int32
   }
 }
 
-// Replay length class of every segment (rays left): 0 done, 1..6 for
-// <= 1, 2, 4, 8, 16, 32 rays, 7 up to kBlockReplayMin, 8 longer.
-// (Also sets each segment's replay cursor: right after its first append, or
-// done -- k_seg_cursor's job, fused.)
-__global__ void k_replay_class(ConsultArgs a, int64_t nseg_cap, uint8_t* cls, int32_t* ids) {
-  const int ns = *a.nsegs;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg_cap;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    int k = 0;
-    if (s < ns) {
-      const int32_t f1 = a.seg_f1[s], end = a.seg_start[s + 1];
-      int32_t cur = end;
-      if (f1 != 0x7fffffff) {  // sidx ascends within a segment: f1's position
-        int32_t lo = a.seg_start[s], hi = end;
-        while (lo < hi) {
-          const int32_t mid = (lo + hi) >> 1;
-          if (a.sidx[mid] < f1) lo = mid + 1;
-          else hi = mid;
-        }
-        cur = lo + 1;
-      }
-      a.seg_cursor[s] = cur;
-      a.seg_napp[s] = f1 != 0x7fffffff ? 1 : 0;
-      const int32_t rem = end - cur;
-      k = rem <= 0 ? 0 : rem <= 1 ? 1 : rem <= 2 ? 2 : rem <= 4 ? 3 : rem <= 8 ? 4
-        : rem <= 16 ? 5 : rem <= 32 ? 6 : rem <= kBlockReplayMin ? 7 : 8;
-    }
-    cls[s] = (uint8_t)k;
-    ids[s] = (int32_t)s;
-  }
-}
 
 // Start of every class in the class-sorted list (9 entries + end).
-__global__ void k_class_bounds(const uint8_t* sorted_cls, int64_t m, int* bounds,
-                               int* bounds_mapped) {
-  const int k = threadIdx.x;
-  if (k > 9) return;
-  int64_t lo = 0, hi = m;  // first position with class >= k
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (sorted_cls[mid] < k) lo = mid + 1;
-    else hi = mid;
+// Replay cursor and length class of every segment (rays left: 0 done,
+// 1..6 for <= 1, 2, 4, 8, 16, 32 rays, 7 up to kBlockReplayMin, 8 longer),
+// binning each segment straight into its class list (order within a class
+// only affects scheduling): per-block shared counters, one global atomic
+// per class per block.
+__global__ void __launch_bounds__(256) k_replay_bin(ConsultArgs a, int64_t cap, int32_t* ids,
+                                                    int* counts, int* counts_mapped) {
+  __shared__ int s_cnt[9], s_base[9];
+  if (threadIdx.x < 9) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int ns = *a.nsegs;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int k = 0, rank = 0;
+  if (s < ns) {
+    const int32_t f1 = a.seg_f1[s], end = a.seg_start[s + 1];
+    int32_t cur = end;
+    if (f1 != 0x7fffffff) {  // sidx ascends within a segment: f1's position
+      int32_t lo = a.seg_start[s], hi = end;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (a.sidx[mid] < f1) lo = mid + 1;
+        else hi = mid;
+      }
+      cur = lo + 1;
+    }
+    a.seg_cursor[s] = cur;
+    a.seg_napp[s] = f1 != 0x7fffffff ? 1 : 0;
+    const int32_t rem = end - cur;
+    k = rem <= 0 ? 0 : rem <= 1 ? 1 : rem <= 2 ? 2 : rem <= 4 ? 3 : rem <= 8 ? 4
+      : rem <= 16 ? 5 : rem <= 32 ? 6 : rem <= kBlockReplayMin ? 7 : 8;
+    if (k > 0) rank = atomicAdd(&s_cnt[k], 1);
   }
-  bounds[k] = (int)lo;
-  if (bounds_mapped) bounds_mapped[k] = (int)lo;
+  __syncthreads();
+  if (threadIdx.x < 9) s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(counts + threadIdx.x,
+                                                                             s_cnt[threadIdx.x])
+                                                                 : 0;
+  __syncthreads();
+  if (k > 0) ids[(int64_t)k * cap + s_base[k] + rank] = (int32_t)s;
 }
+
+__global__ void k_counts_to_host(const int* counts, int* mapped) {
+  if (threadIdx.x < 9) mapped[threadIdx.x] = counts[threadIdx.x];
+}
+
 
 // Flags of the active segments longer than short_len.
 __global__ void k_long_flags(ConsultArgs a, int64_t n, int short_len, uint8_t* flags) {
@@ -927,32 +928,21 @@ static SidePool& side_pool() {
 
 template <bool CLOSEST, bool LIVE, int STACK>
 static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, int64_t nseg_cap) {
-  uint8_t *cls, *cls_sorted;
-  int32_t *ids, *ids_sorted;
+  int32_t* ids;  // class k's segments at ids[k * m ...]
+  int* ct;       // [0, 10) per-class counts, [10, 20) per-class tickets
   int rc;
   const int64_t m = nseg_cap > 0 ? nseg_cap : 1;
-  if ((rc = ws.get("rg_cls", m, &cls)) || (rc = ws.get("rg_cls2", m, &cls_sorted)) ||
-      (rc = ws.get("rg_ids", m, &ids)) || (rc = ws.get("rg_ids2", m, &ids_sorted)))
-    return rc;
-  k_replay_class<<<grid_for(m, 256, num_sms() * 8), 256, 0, st>>>(a, m, cls, ids);
-  HRPP_LAUNCHED();
-  size_t b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 4, st);
-  void* tmp;
-  if ((rc = ws.get_raw("rg_tmp", b, &tmp))) return rc;
-  HRPP_CK(cub::DeviceRadixSort::SortPairs(tmp, b, cls, cls_sorted, ids, ids_sorted, (int)m, 0, 4,
-                                          st));
-  int hb[10];
+  if ((rc = ws.get("rg_idsbin", 9 * m, &ids)) || (rc = ws.get("rg_ct", 20, &ct))) return rc;
+  int* counts = ct;
+  int* tickets = ct + 10;
+  HRPP_CK(cudaMemsetAsync(ct, 0, sizeof(int) * 20, st));
   long long* pin = pinned_scratch();
   if (!pin) return HRPP_CUDA;
-  int *bounds, *tickets;
-  if ((rc = ws.get("rg_bounds", 10, &bounds)) || (rc = ws.get("rg_tickets", 10, &tickets)))
-    return rc;
-  HRPP_CK(cudaMemsetAsync(tickets, 0, sizeof(int) * 10, st));
-  // class bounds to the device (read there by the class kernels) and to this
-  // thread's mapped pinned buffer (the host needs only class 8's count,
-  // waited for behind an event once classes 1-7 are queued)
-  k_class_bounds<<<1, 32, 0, st>>>(cls_sorted, m, bounds, reinterpret_cast<int*>(pin + 40));
+  k_replay_bin<<<(int)((m + 255) / 256), 256, 0, st>>>(a, m, ids, counts, nullptr);
+  HRPP_LAUNCHED();
+  // the host needs only class 8's count, read through mapped memory behind
+  // an event once classes 1-7 are queued
+  k_counts_to_host<<<1, 32, 0, st>>>(counts, reinterpret_cast<int*>(pin + 40));
   HRPP_LAUNCHED();
   const cudaEvent_t ev_cls = side_pool().cls_ready;
   HRPP_CK(cudaEventRecord(ev_cls, st));
@@ -978,7 +968,7 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
   };
 #define HRPP_GROUP(K, GS)                                                                     \
   k_replay_group<CLOSEST, LIVE, STACK, GS><<<pgrid(128 / GS, 6), 128, 0, side(K)>>>(         \
-      a, ids_sorted, bounds, K, tickets + K);                                                 \
+      a, ids, counts, m, K, tickets + K);                                                     \
   HRPP_LAUNCHED();
   HRPP_GROUP(1, 1)
   HRPP_GROUP(2, 2)
@@ -989,11 +979,13 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
 #undef HRPP_GROUP
   // long segments: a warp each, 32-ray tiles
   k_replay_block<CLOSEST, LIVE, STACK, 32><<<pgrid(1, HRPP_BLOCK32_MINB), 32, 0, side(7)>>>(
-      a, ids_sorted, 0, bounds, 7, tickets + 7);
+      a, ids, 0, counts, m, 7, tickets + 7);
   HRPP_LAUNCHED();
   HRPP_CK(cudaEventSynchronize(ev_cls));
-  memcpy(hb, (const void*)(pin + 40), sizeof(int) * 10);
-  auto cnt = [&](int k) { return hb[k + 1] - hb[k]; };
+  int hb[10];
+  memcpy(hb, (const void*)(pin + 40), sizeof(int) * 9);
+  auto cnt = [&](int k) { return hb[k]; };
+  const int32_t* ids8_in = ids + 8 * m;
   // class 8 below runs on st after the join (it sorts by remaining length)
   for (int k = 0; k < HRPP_REPLAY_STREAMS; k++)
     if (used & (1 << k)) {
@@ -1006,18 +998,17 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
     if ((rc = ws.get("rg_rem", c8, &rem)) || (rc = ws.get("rg_rem2", c8, &rem2)) ||
         (rc = ws.get("rg_ids8", c8, &ids8)))
       return rc;
-    k_seg_remaining<<<grid_for(c8, 256, num_sms() * 4), 256, 0, st>>>(a, ids_sorted + hb[8], c8,
-                                                                       rem);
+    k_seg_remaining<<<grid_for(c8, 256, num_sms() * 4), 256, 0, st>>>(a, ids8_in, c8, rem);
     HRPP_LAUNCHED();
     size_t b8 = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, b8, rem, rem2, ids_sorted + hb[8], ids8,
-                                              c8, 0, 32, st);
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, b8, rem, rem2, ids8_in, ids8, c8, 0, 32,
+                                              st);
     void* tmp8;
     if ((rc = ws.get_raw("rg_tmp8", b8, &tmp8))) return rc;
-    HRPP_CK(cub::DeviceRadixSort::SortPairsDescending(tmp8, b8, rem, rem2, ids_sorted + hb[8],
-                                                      ids8, c8, 0, 32, st));
+    HRPP_CK(cub::DeviceRadixSort::SortPairsDescending(tmp8, b8, rem, rem2, ids8_in, ids8, c8, 0,
+                                                      32, st));
     k_replay_block<CLOSEST, LIVE, STACK, kBlockReplay><<<c8, kBlockReplay, 0, st>>>(
-        a, ids8, c8, nullptr, 0, nullptr);
+        a, ids8, c8, nullptr, 0, 0, nullptr);
     HRPP_LAUNCHED();
   }
   return 0;
@@ -1089,7 +1080,7 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
     else k_finalize<false, false><<<fgrid, 128, 0, st>>>(a, n);
   }
   HRPP_LAUNCHED();
-  return 0;  // the replay cursors are set by k_replay_class
+  return 0;  // the replay cursors are set by k_replay_bin
 }
 
 int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* keys,
