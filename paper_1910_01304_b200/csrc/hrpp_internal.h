@@ -192,7 +192,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
 int table_record(TableDev& t, const uint64_t* keys, const int32_t* nodes, int64_t n,
                  uint8_t* inserted, int* err, cudaStream_t st);
 int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
-                 int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st);
+                 int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st,
+                 const int32_t* seg_cursor = nullptr);
 int table_collect_pending(TableDev& t, const Segments& seg, int64_t n, const int32_t* seg_napp,
                           const int32_t* app, const int32_t* app_ray, int* err,
                           cudaStream_t st);

@@ -1285,9 +1285,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     } else {
       if ((rc = launch_replay(t.closest, true, b.stack, st, a, ws, LL, n))) return rc;
     }
-    k_check_done<<<grid_for(n, 256, num_sms() * 4), 256, 0, st>>>(seg.nsegs, seg.seg_start,
-                                                                 a.seg_cursor, err);
-    HRPP_LAUNCHED();
+    // (every segment replayed to its end: checked by k_commit_count, or below
+    // in deferred mode)
   } else {
     a.f_found = c.base_found;
     a.f_t = c.base_t;
@@ -1308,10 +1307,17 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     if ((rc = launch_grouped(t.closest, false, b.stack, st, a, ws, nsegs_h))) return rc;
   }
   if ((rc = resolve_nsegs())) return rc;
-  if (t.deferred)
+  if (t.deferred) {
+    if (c.live) {
+      k_check_done<<<grid_for(n, 256, num_sms() * 4), 256, 0, st>>>(seg.nsegs, seg.seg_start,
+                                                                   a.seg_cursor, err);
+      HRPP_LAUNCHED();
+    }
     return table_collect_pending(t, seg, n, a.seg_napp, a.app, a.app_ray, err, st);
+  }
   // one thread per key segment (nsegs_h of them), not per ray
-  return table_commit(t, seg, nsegs_h, a.seg_eid, a.seg_napp, a.app, err, st);
+  return table_commit(t, seg, nsegs_h, a.seg_eid, a.seg_napp, a.app, err, st,
+                      c.live ? a.seg_cursor : nullptr);
 }
 
 }  // namespace hrpp

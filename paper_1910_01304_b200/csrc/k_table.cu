@@ -464,9 +464,13 @@ __global__ void __launch_bounds__(128) k_commit_count(const int* nsegs,
                                                       const int32_t* __restrict__ seg_eid,
                                                       const int32_t* __restrict__ seg_napp,
                                                       const int32_t* __restrict__ e_len,
-                                                      Tot3* block_tot, const int* err) {
+                                                      Tot3* block_tot, int* err,
+                                                      const int32_t* __restrict__ seg_start,
+                                                      const int32_t* __restrict__ seg_cursor) {
   if (*err) return;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // (consult) every segment replayed to its end, else an internal error
+  if (seg_cursor && s < *nsegs && seg_cursor[s] < seg_start[s + 1]) atomicCAS(err, 0, 4);
   int32_t napp, eid, old_len;
   seg_commit_counts(*nsegs, s, seg_eid, seg_napp, e_len, napp, eid, old_len);
   long long ex_new, ex_reloc, t_new, t_reloc;
@@ -526,7 +530,8 @@ __global__ void k_commit_finish(long long* meta, const Tot3* total, const int* e
 }
 
 int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
-                 int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st) {
+                 int32_t* seg_napp, const int32_t* app, int* err, cudaStream_t st,
+                 const int32_t* seg_cursor) {
   const int nblocks = (int)((n + 127) / 128);
   Tot3 *btot, *boff, *total;
   int rc;
@@ -538,7 +543,8 @@ int table_commit(TableDev& t, const Segments& seg, int64_t n, int32_t* seg_eid,
   void* tmp;
   if ((rc = t.ws.get_raw("m_tmp", b, &tmp))) return rc;
   ProfScope ps(P_COMMIT, st);
-  k_commit_count<<<nblocks, 128, 0, st>>>(seg.nsegs, seg_eid, seg_napp, t.e_len, btot, err);
+  k_commit_count<<<nblocks, 128, 0, st>>>(seg.nsegs, seg_eid, seg_napp, t.e_len, btot, err,
+                                          seg.seg_start, seg_cursor);
   HRPP_LAUNCHED();
   HRPP_CK(cub::DeviceScan::ExclusiveScan(tmp, b, btot, boff, Tot3Sum(), Tot3{0, 0, 0}, nblocks,
                                          st));
