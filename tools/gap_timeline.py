@@ -10,6 +10,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 import paper_1910_01304_b200 as hb  # noqa: E402
 
+TL = "--timeline" in sys.argv
+sys.argv = [a for a in sys.argv if a != "--timeline"]
 args = bench.parse()
 sc, bvh, waves = bench.make_workload(args, trace_closest=lambda b, O, D, t0, t1:
                                      hb.intersect_closest_batch(b, O, D, t0, t1))
@@ -51,3 +53,10 @@ tot = sum(g[0] for g in gaps)
 print(f"frame span {(t1 - t0) / 1e3:.3f} ms, {len(ev)} activities, idle {tot / 1e3:.3f} ms in {len(gaps)} gaps")
 for g in sorted(gaps, reverse=True)[:25]:
     print(f"{g[0]:8.1f} us  after {g[1]:60s} before {g[2]}")
+
+if TL:
+    print("\n# start_us  dur_us  kernel (one frame, all streams)")
+    for s, e, n in ev:
+        d = (e - s)
+        if d >= 15:
+            print(f"{(s - t0):9.1f} {d:8.1f}  {n}")
