@@ -36,6 +36,9 @@ namespace hrpp {
 #ifndef HRPP_BOX32
 #define HRPP_BOX32 1
 #endif
+#ifndef HRPP_SLAB_MINMAX
+#define HRPP_SLAB_MINMAX 1
+#endif
 #ifndef HRPP_LDG256
 #define HRPP_LDG256 1
 #endif
@@ -350,6 +353,19 @@ static __device__ __noinline__ bool box_hit_exact(float lx, float ly, float lz, 
 // float64 test.  The result is therefore always the reference's.
 __device__ __forceinline__ bool box_hit32(const NodeBox32& n, const Ray& r, uint32_t ivneg,
                                           float t1f, double t1) {
+#if HRPP_SLAB_MINMAX
+  // Slab entry/exit by min/max instead of swapping on the sign of 1/d: the
+  // same values whenever no slab value is NaN (rounding is monotone, so the
+  // smaller of the two is the one the swap picks); with a NaN (d = 0 and the
+  // origin on that slab plane) the two differ only by putting an infinity
+  // into tn or tf, which sends the test to the float64 path below.
+  (void)ivneg;
+  const float lx = (n.lx - r.ox) * r.ivx, hx = (n.hx - r.ox) * r.ivx;
+  const float ly = (n.ly - r.oy) * r.ivy, hy = (n.hy - r.oy) * r.ivy;
+  const float lz = (n.lz - r.oz) * r.ivz, hz = (n.hz - r.oz) * r.ivz;
+  const float tn = fmaxf(fmaxf(r.t0f, fminf(lx, hx)), fmaxf(fminf(ly, hy), fminf(lz, hz)));
+  const float tf = fminf(fminf(t1f, fmaxf(lx, hx)), fminf(fmaxf(ly, hy), fmaxf(lz, hz)));
+#else
   const float nx = (ivneg & 1u) ? n.hx : n.lx, fx = (ivneg & 1u) ? n.lx : n.hx;
   const float ny = (ivneg & 2u) ? n.hy : n.ly, fy = (ivneg & 2u) ? n.ly : n.hy;
   const float nz = (ivneg & 4u) ? n.hz : n.lz, fz = (ivneg & 4u) ? n.lz : n.hz;
@@ -358,6 +374,7 @@ __device__ __forceinline__ bool box_hit32(const NodeBox32& n, const Ray& r, uint
   const float az = (nz - r.oz) * r.ivz, bz = (fz - r.oz) * r.ivz;
   const float tn = fmaxf(fmaxf(r.t0f, ax), fmaxf(ay, az));
   const float tf = fminf(fminf(t1f, bx), fminf(by, bz));
+#endif
   const float d = tf - tn;
   const float m = __fmaf_ru(fabsf(tn) + fabsf(tf), 0x1p-18f, 0x1p-126f);
   if (d > m) return true;
