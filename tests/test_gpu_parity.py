@@ -828,3 +828,11 @@ def test_table_clear_reuse_equals_fresh(hb):
         assert gd == rd
         for k in ro:
             assert np.array_equal(go[k], ro[k]), k
+    # host (numpy) arrays after a clear on an explicit stream
+    side = torch.cuda.Stream()
+    used.clear(stream=side)
+    side.synchronize()
+    out_h, st_h = hb.trace_wave(b, used, "live", O, D, np.zeros(n), np.full(n, np.inf), True)
+    assert np.array_equal(st_h, ref[0][1])
+    for k in ref[0][0]:
+        assert np.array_equal(np.asarray(out_h[k]), ref[0][0][k]), k
