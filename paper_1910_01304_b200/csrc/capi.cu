@@ -393,7 +393,7 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
                     const int32_t* tri_ids, int64_t n_nodes, int64_t n_tris, int device,
                     hrpp_bvh_t* out) {
   (void)tri_ids;
-  CHECK_ARG(n_nodes >= 1 && n_nodes < (1LL << 30), "node count must be in [1, 2^30)");
+  CHECK_ARG(n_nodes >= 1 && n_nodes < (1LL << 27), "node count must be in [1, 2^27)");
   CHECK_ARG(n_tris >= 0 && n_tris < (1LL << 31), "triangle count out of range");
   HRPP_CK(cudaSetDevice(device));
   std::vector<DNode> hn(n_nodes);
@@ -407,7 +407,7 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
                 "child index out of range");
       int ax = axis[i] == 1 ? 1 : (axis[i] == 2 ? 2 : 0);
       pack_node(hn[i], bmin + 3 * i, bmax + 3 * i, left[i],
-                (int32_t)((uint32_t)right[i] | ((uint32_t)ax << 30)));
+                (int32_t)((uint32_t)right[i] | (1u << (27 + ax))));
     }
   }
   // tree height from the root (stack bound); guards against cycles

@@ -2,7 +2,7 @@
 //
 // Layout in HBM:
 //   DNode  64 B  {double lo.xyz, hi.xyz; a, b}: four 16-B loads per visit.
-//          interior: a = left (>= 0), b = right | axis << 30
+//          interior: a = left (>= 0), b = right | 1 << (27 + axis)
 //          leaf:     a = ~first (< 0, so the reference's `left < 0` test
 //                    becomes `a < 0`), b = count
 //   DTri   80 B  {double v0.xyz v1.xyz v2.xyz}: five loads.
@@ -439,6 +439,12 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
 #if HRPP_OPAQUE_SIGNS
   asm volatile("mov.u32 %0, %0;" : "+r"(ivneg));  // keep the bits, not 3 float64 compares
 #endif
+  // d[axis] < 0 at bit 27 + axis, matching the interior nodes' axis bit
+#if HRPP_BOX32
+  const uint32_t dmask = (ivneg & 0x38u) << 24;
+#else
+  const uint32_t dmask = dneg << 27;
+#endif
   // h.t starts at tmax for both kinds: the closest-hit box interval is
   // [tmin, best t] and a hit needs t <= tmax before the first hit and
   // t < best t after it; an any-hit ray's interval stays [tmin, tmax] until
@@ -463,13 +469,9 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
       const int32_t a = nb.a;
       const int32_t b = nb.b;
       if (a >= 0) {
-        const uint32_t axis = (uint32_t)b >> 30;
-        const int32_t right = b & 0x3FFFFFFF;
-#if HRPP_BOX32
-        const bool go_right = (ivneg >> (axis + 3)) & 1u;
-#else
-        const bool go_right = (dneg >> axis) & 1u;
-#endif
+        // b = right | 1 << (27 + axis): one AND against the ray's sign mask
+        const int32_t right = b & 0x07FFFFFF;
+        const bool go_right = ((uint32_t)b & dmask) != 0u;
         stack[top++] = go_right ? a : right;  // far
         nd = go_right ? right : a;             // near, visited next
         continue;
