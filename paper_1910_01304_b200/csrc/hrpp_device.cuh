@@ -1,14 +1,20 @@
-// hrpp_device.cuh -- device data layout and the bit-exact f64 traversal core.
+// hrpp_device.cuh -- device data layout and the bit-exact traversal core.
 //
 // Layout in HBM:
-//   DNode  64 B  {double lo.xyz, hi.xyz; a, b}: four 16-B loads per visit.
+//   DNode  32 B  {float lo.xyz; a; float hi.xyz; b}: one 256-bit load per
+//          visit (the reference's float32 boxes, exact in float64).
 //          interior: a = left (>= 0), b = right | 1 << (27 + axis)
 //          leaf:     a = ~first (< 0, so the reference's `left < 0` test
 //                    becomes `a < 0`), b = count
-//   DTri   80 B  {double v0.xyz v1.xyz v2.xyz}: five loads.
-//   (HRPP_NODE_F64=0: 32-B / 48-B float32 records, widened on load.)
+//   DTri   96 B  {double v0.xyz, e1.xyz, e2.xyz; leaf}: the reference's
+//          float64 vertex and edges (e = v - v0 rounded once, as it does per
+//          test), two 256-bit loads and one 64-bit load.
+//   (HRPP_BOX32=0 / HRPP_NODE_F64=0: the earlier float64-node and
+//   float32-triangle layouts, kept for experiments.)
 //
-// Arithmetic restates hrpp/kernels.py:23-206 operation by operation in
+// Arithmetic restates hrpp/kernels.py:23-206 operation by operation: the
+// slab test runs in float32 with a certified error margin and falls back to
+// the reference's float64 test inside it (box_hit32); the triangle test is
 // float64.  The whole library is compiled with --fmad=false so no
 // multiply-add is contracted (numba emits none either), and double division
 // is IEEE round-to-nearest, so results are bit-identical to the reference.
