@@ -284,10 +284,10 @@ struct TraceArgs {
   TraceOut out;
 };
 
-// Register cap from the resident-block target: 7 x 128 threads -> 72
-// registers (measured best of 1, 5, 6, 7, 8 on c2: +6 % primary, +8 %
-// shadow, +13 % bounce over the uncapped 86).  A leaf-batched "while-while"
-// loop (warp-synchronous box and triangle phases) measured 40 % slower.
+// Register cap from the resident-block target: 8 x 128 threads -> 64
+// registers, no spills with the float32 slab test (measured against 6, 7, 9
+// and 10 blocks on c2).  Warp-synchronous variants (leaf batching,
+// cooperative leaves) measured 25-90 % slower; see DESIGN.md section 8.
 #ifndef HRPP_TRACE_MINB
 #define HRPP_TRACE_MINB 8
 #endif
