@@ -305,7 +305,8 @@ __global__ void k_first_append(ConsultArgs a, int64_t n) {
     if (ex_len > 0 && a.state[i].found) continue;  // TP against the wave-start entry
     if (a.f_known && !a.f_known[i]) continue;  // (live) no full result: never a first append
     if (!a.f_found[i]) continue;
-    if (!in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[i]]))
+    // (no entry: every hit appends -- skip the leaf and ancestor reads)
+    if (ex_len == 0 || !in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[i]]))
       atomicMin(a.seg_f1 + s, (int32_t)i);
   }
 }
