@@ -288,12 +288,15 @@ struct TraceArgs {
 // registers, no spills with the float32 slab test (measured against 6, 7, 9
 // and 10 blocks on c2).  Warp-synchronous variants (leaf batching,
 // cooperative leaves) measured 25-90 % slower; see DESIGN.md section 8.
+#ifndef HRPP_TRACE_BS
+#define HRPP_TRACE_BS 32  // one warp per block: a warp frees its slot as soon as its own rays finish
+#endif
 #ifndef HRPP_TRACE_MINB
 #define HRPP_TRACE_MINB 8
 #endif
 
 template <bool CLOSEST, int STACK>
-__global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
+__global__ void __launch_bounds__(HRPP_TRACE_BS, HRPP_TRACE_MINB * 128 / HRPP_TRACE_BS) k_trace(TraceArgs a) {
   if (a.err && *a.err) return;
   // one ray per thread; with a device-side count (fallback queue) the grid is
   // sized for the host-known upper bound and surplus threads exit at once
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     stt = h.tris;
   }
   if (a.out.sums) {  // one atomic pair per block (a.out.sums is uniform)
-    __shared__ unsigned long long part[2][4];
+    __shared__ unsigned long long part[2][HRPP_TRACE_BS / 32];
     sb = warp_sum(sb);
     stt = warp_sum(stt);
     if ((threadIdx.x & 31) == 0) {
@@ -343,8 +346,9 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
     }
     __syncthreads();
     if (threadIdx.x < 2) {
-      const unsigned long long v = part[threadIdx.x][0] + part[threadIdx.x][1] +
-                                   part[threadIdx.x][2] + part[threadIdx.x][3];
+      unsigned long long v = 0;
+#pragma unroll
+      for (int w = 0; w < HRPP_TRACE_BS / 32; w++) v += part[threadIdx.x][w];
       if (v) atomicAdd(a.out.sums + threadIdx.x, v);
     }
   }
@@ -353,11 +357,11 @@ __global__ void __launch_bounds__(128, HRPP_TRACE_MINB) k_trace(TraceArgs a) {
 template <bool CLOSEST>
 static void dispatch_trace(int stack, int grid, cudaStream_t st, const TraceArgs& a) {
   switch (stack) {
-    case 32: k_trace<CLOSEST, 32><<<grid, 128, 0, st>>>(a); break;
-    case 64: k_trace<CLOSEST, 64><<<grid, 128, 0, st>>>(a); break;
-    case 128: k_trace<CLOSEST, 128><<<grid, 128, 0, st>>>(a); break;
-    case 256: k_trace<CLOSEST, 256><<<grid, 128, 0, st>>>(a); break;
-    default: k_trace<CLOSEST, 512><<<grid, 128, 0, st>>>(a); break;
+    case 32: k_trace<CLOSEST, 32><<<grid, HRPP_TRACE_BS, 0, st>>>(a); break;
+    case 64: k_trace<CLOSEST, 64><<<grid, HRPP_TRACE_BS, 0, st>>>(a); break;
+    case 128: k_trace<CLOSEST, 128><<<grid, HRPP_TRACE_BS, 0, st>>>(a); break;
+    case 256: k_trace<CLOSEST, 256><<<grid, HRPP_TRACE_BS, 0, st>>>(a); break;
+    default: k_trace<CLOSEST, 512><<<grid, HRPP_TRACE_BS, 0, st>>>(a); break;
   }
 }
 
@@ -369,7 +373,7 @@ int launch_trace(const BvhDev& b, bool closest, const float* O, const float* D,
   if (n <= 0) return 0;
   TraceArgs a{b.nodes, b.tris, O, D, tmin, tmax, start, n, ray_idx, count_dev, err, out};
   ProfScope ps(ray_idx || fallback ? P_TRACE_QUEUE : P_TRACE, st);
-  const int grid = (int)((n + 127) / 128);
+  const int grid = (int)((n + HRPP_TRACE_BS - 1) / HRPP_TRACE_BS);
   if (closest) dispatch_trace<true>(b.stack, grid, st, a);
   else dispatch_trace<false>(b.stack, grid, st, a);
   HRPP_LAUNCHED();
