@@ -265,6 +265,9 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
 #ifndef HRPP_REPLAY_MINB
 #define HRPP_REPLAY_MINB 6  // 80 registers (measured: consult 4.66 -> 4.11 ms on c2)
 #endif
+#ifndef HRPP_REPLAY_BS
+#define HRPP_REPLAY_BS 32  // k_replay_group block size (warps take tickets on their own)
+#endif
 
 __global__ void k_seg_lookup(ConsultArgs a, int64_t n) {
   const int ns = *a.nsegs;
@@ -557,26 +560,26 @@ __global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_long(ConsultAr
 // with at most G rays left (the rays after its first append), 32/G segments
 // per warp.  Within a group this is seg_warp's ballot loop.
 template <bool CLOSEST, bool LIVE, int STACK, int G>
-__global__ void __launch_bounds__(128, HRPP_REPLAY_MINB) k_replay_group(ConsultArgs a, const int32_t* ids,
-                                                      const int* counts, int64_t cap, int K,
-                                                      int* ticket) {
+__global__ void __launch_bounds__(HRPP_REPLAY_BS, HRPP_REPLAY_MINB * 128 / HRPP_REPLAY_BS)
+    k_replay_group(ConsultArgs a, const int32_t* ids, const int* counts, int64_t cap, int K,
+                   int* ticket) {
   if (*a.err) return;
-  // Persistent blocks take 128 / G segments at a time from the class's
-  // ticket; the class (list, count) is read on the device, so the host
-  // launches without waiting for the class bounds.
+  // Persistent warps take 32 / G segments at a time from the class's ticket
+  // (each warp on its own: no warp waits for a slower one in its block); the
+  // class (list, count) is read on the device, so the host launches without
+  // waiting for the class bounds.
   const int32_t* list = ids + (int64_t)K * cap;
   const int count = counts[K];
   const int lane = threadIdx.x & 31;
   const int gl = lane % G, gbase = lane - gl;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase);
   Tally c;
-  __shared__ int s_base;
   for (;;) {
-  __syncthreads();  // s_base of the previous batch read by every thread
-  if (threadIdx.x == 0) s_base = atomicAdd(ticket, 128 / G);
-  __syncthreads();
-  if (s_base >= count) break;
-  const int gid = s_base + (int)threadIdx.x / G;
+  int wbase = 0;
+  if (lane == 0) wbase = atomicAdd(ticket, 32 / G);
+  wbase = __shfl_sync(kFull, wbase, 0);
+  if (wbase >= count) break;
+  const int gid = wbase + lane / G;
   const bool gvalid = gid < count;
   int s = 0;
   int32_t beg = 0, end = 0, tb = 0, napp = 0, ex_len = 0;
@@ -968,8 +971,9 @@ static int grouped_impl(cudaStream_t st, const ConsultArgs& a, Workspace& ws, in
     return (int)(need < cap ? (need > 0 ? need : 1) : cap);
   };
 #define HRPP_GROUP(K, GS)                                                                     \
-  k_replay_group<CLOSEST, LIVE, STACK, GS><<<pgrid(128 / GS, 6), 128, 0, side(K)>>>(         \
-      a, ids, counts, m, K, tickets + K);                                                     \
+  k_replay_group<CLOSEST, LIVE, STACK, GS>                                                    \
+      <<<pgrid(HRPP_REPLAY_BS / GS, 6 * 128 / HRPP_REPLAY_BS), HRPP_REPLAY_BS, 0, side(K)>>>( \
+          a, ids, counts, m, K, tickets + K);                                                 \
   HRPP_LAUNCHED();
   HRPP_GROUP(1, 1)
   HRPP_GROUP(2, 2)
