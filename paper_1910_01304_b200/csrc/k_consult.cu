@@ -265,6 +265,9 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
 #ifndef HRPP_REPLAY_MINB
 #define HRPP_REPLAY_MINB 6  // 80 registers (measured: consult 4.66 -> 4.11 ms on c2)
 #endif
+#ifndef HRPP_EVAL_BS
+#define HRPP_EVAL_BS 128  // k_eval0 block size (32 measured slower)
+#endif
 #ifndef HRPP_REPLAY_BS
 #define HRPP_REPLAY_BS 32  // k_replay_group block size (warps take tickets on their own)
 #endif
@@ -345,7 +348,8 @@ __global__ void __launch_bounds__(128, HRPP_FIN_MINB) k_finalize(ConsultArgs a, 
 // data coalesced, one random 4-B store per ray); only rays whose key already
 // had an entry read their ray and evaluate it.
 template <bool CLOSEST, int STACK>
-__global__ void __launch_bounds__(128, HRPP_EVAL_MINB) k_eval0(ConsultArgs a, int64_t n, int mark_need) {
+__global__ void __launch_bounds__(HRPP_EVAL_BS, HRPP_EVAL_MINB * 128 / HRPP_EVAL_BS)
+    k_eval0(ConsultArgs a, int64_t n, int mark_need) {
   if (*a.err) return;
   unsigned long long tps = 0;  // wave-start TPs (the early-traversal policy)
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
@@ -1059,10 +1063,12 @@ static void dispatch_eval0(int stack, int grid, cudaStream_t st, const ConsultAr
                                                                     a.seg_of_ray);
     return;
   }
+  (void)grid;
+  const int egrid = (int)((n + HRPP_EVAL_BS - 1) / HRPP_EVAL_BS);
   switch (stack) {
-    case 64: k_eval0<CLOSEST, 64><<<grid, 128, 0, st>>>(a, n, mark); break;
-    case 256: k_eval0<CLOSEST, 256><<<grid, 128, 0, st>>>(a, n, mark); break;
-    default: k_eval0<CLOSEST, 512><<<grid, 128, 0, st>>>(a, n, mark); break;
+    case 64: k_eval0<CLOSEST, 64><<<egrid, HRPP_EVAL_BS, 0, st>>>(a, n, mark); break;
+    case 256: k_eval0<CLOSEST, 256><<<egrid, HRPP_EVAL_BS, 0, st>>>(a, n, mark); break;
+    default: k_eval0<CLOSEST, 512><<<egrid, HRPP_EVAL_BS, 0, st>>>(a, n, mark); break;
   }
 }
 
