@@ -265,6 +265,12 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
 #ifndef HRPP_REPLAY_MINB
 #define HRPP_REPLAY_MINB 6  // 80 registers (measured: consult 4.66 -> 4.11 ms on c2)
 #endif
+#ifndef HRPP_FIN_BS
+#define HRPP_FIN_BS 128  // k_finalize block size
+#endif
+#ifndef HRPP_FA_BS
+#define HRPP_FA_BS 256  // k_first_append block size
+#endif
 #ifndef HRPP_EVAL_BS
 #define HRPP_EVAL_BS 128  // k_eval0 block size (32 measured slower)
 #endif
@@ -318,7 +324,8 @@ __global__ void k_first_append(ConsultArgs a, int64_t n) {
 }
 
 template <bool CLOSEST, bool LIVE>
-__global__ void __launch_bounds__(128, HRPP_FIN_MINB) k_finalize(ConsultArgs a, int64_t n) {
+__global__ void __launch_bounds__(HRPP_FIN_BS, HRPP_FIN_MINB * 128 / HRPP_FIN_BS)
+    k_finalize(ConsultArgs a, int64_t n) {
   if (*a.err) return;
   Tally c;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1076,19 +1083,20 @@ static int finalize_prefix(bool closest, bool live, int grid, cudaStream_t st,
                            const ConsultArgs& a, int64_t n, bool first_append_done = false) {
   ProfScope ps(P_CONSULT, st);
   if (!first_append_done) {
-    k_first_append<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a, n);
+    k_first_append<<<grid_for(n, HRPP_FA_BS, num_sms() * 16 * 256 / HRPP_FA_BS), HRPP_FA_BS, 0,
+                     st>>>(a, n);
     HRPP_LAUNCHED();
   }
   // about one resident wave of blocks: a thread walks several rays and each
   // block flushes its tallies once
-  const int fgrid = grid_for(n, 128, num_sms() * HRPP_FIN_GRID);
+  const int fgrid = grid_for(n, HRPP_FIN_BS, num_sms() * HRPP_FIN_GRID * 128 / HRPP_FIN_BS);
   (void)grid;
   if (closest) {
-    if (live) k_finalize<true, true><<<fgrid, 128, 0, st>>>(a, n);
-    else k_finalize<true, false><<<fgrid, 128, 0, st>>>(a, n);
+    if (live) k_finalize<true, true><<<fgrid, HRPP_FIN_BS, 0, st>>>(a, n);
+    else k_finalize<true, false><<<fgrid, HRPP_FIN_BS, 0, st>>>(a, n);
   } else {
-    if (live) k_finalize<false, true><<<fgrid, 128, 0, st>>>(a, n);
-    else k_finalize<false, false><<<fgrid, 128, 0, st>>>(a, n);
+    if (live) k_finalize<false, true><<<fgrid, HRPP_FIN_BS, 0, st>>>(a, n);
+    else k_finalize<false, false><<<fgrid, HRPP_FIN_BS, 0, st>>>(a, n);
   }
   HRPP_LAUNCHED();
   return 0;  // the replay cursors are set by k_replay_bin
