@@ -466,9 +466,13 @@ def test_train_from_traversal_go_up(hb):
 
 # -- full-size properties ----------------------------------------------------------------
 
-def test_c1_frame_vs_oracle(hb, oracle_mod):
-    """BASELINE config c1 end to end (primary, shadow, bounce waves) in limit
-    and live mode: GPU == C oracle on every output, stat and table dump."""
+@pytest.mark.parametrize("p,g_", [(6, 0), (4, 2), (5, 1)])
+def test_c1_frame_vs_oracle(hb, oracle_mod, p, g_):
+    """BASELINE config c1 end to end (primary, shadow, bounce waves, then a
+    second bounce wave on the populated closest-hit table) in limit and live
+    mode, at several precisions and go-up levels: GPU == C oracle on every
+    output, stat and table dump (early traversal, wave-start TPs, replay
+    classes and go-up subtree evaluation all on the path)."""
     from paper_1910_01304_b200 import scenes
     sc = scenes.make_scene("c1")
     b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
@@ -482,11 +486,12 @@ def test_c1_frame_vs_oracle(hb, oracle_mod):
     lights = np.broadcast_to(np.array(sc.point_lights[0]), P.shape)
     waves = [(True, O, D, np.zeros(n), np.full(n, np.inf)),
              (False, *scenes.shadow_rays(P, lights)),
-             (True, *scenes.cosine_bounce(P, N, seed=0))]
+             (True, *scenes.cosine_bounce(P, N, seed=0)),
+             (True, O, D, np.zeros(n), np.full(n, np.inf))]
     for mode in ("limit", "live"):
-        tabs = {c: hb.PredictorTable(hb.HashConfig(6), 0, hb.RayKind.CLOSEST_HIT if c
+        tabs = {c: hb.PredictorTable(hb.HashConfig(p), g_, hb.RayKind.CLOSEST_HIT if c
                                      else hb.RayKind.HIT_ANY) for c in (True, False)}
-        otabs = {c: oracle_mod.OracleTable(6, 0, c) for c in (True, False)}
+        otabs = {c: oracle_mod.OracleTable(p, g_, c) for c in (True, False)}
         for closest, Ow, Dw, t0, t1 in waves:
             out, st = hb.trace_wave(b, tabs[closest], mode, Ow, Dw, t0, t1, closest,
                                     capture_outcomes=True)
