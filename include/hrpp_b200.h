@@ -95,6 +95,10 @@ int hrpp_hash_rays(const float *O, const float *D, int64_t n, int p, uint64_t *k
                    void *stream);
 /* hrpp/rayhash.py:67-78 map_float_to_hash over a float32 array. */
 int hrpp_hash_floats(const float *f, int64_t n, int p, uint32_t *out, void *stream);
+/* hrpp/rayhash.py:125-147 coarsen_key: 48-bit keys at precision p -> the
+ * keys of the same rays at p - 1 (p in [2, 7]), computed per lane on the
+ * device (host or device arrays). */
+int hrpp_coarsen_keys(const uint64_t *keys, int64_t n, int p, uint64_t *out, void *stream);
 
 /* ---- BVH: hrpp/bvh.py:75-92 (Bvh(...)) and the 10-array kernel ABI of
  * hrpp/bvh.py:126-128, plus parent/depth (predictor) and tri_ids.  Host

@@ -59,6 +59,7 @@ def _load():
     L.hrpp_profile_read.argtypes = [P, P, C.c_int, C.c_int]
     L.hrpp_hash_rays.argtypes = [P, P, I64, C.c_int, P, P]
     L.hrpp_hash_floats.argtypes = [P, I64, C.c_int, P, P]
+    L.hrpp_coarsen_keys.argtypes = [P, I64, C.c_int, P, P]
     L.hrpp_bvh_create.argtypes = [P] * 13 + [I64, I64, C.c_int, P]
     L.hrpp_bvh_destroy.argtypes = [P]
     L.hrpp_bvh_ancestor_lut.argtypes = [P, C.c_int, P]
@@ -83,7 +84,7 @@ def _load():
     L.hrpp_trace_wave.argtypes = [P, P, C.c_int, C.c_int, P, P, P, P, I64, C.POINTER(WaveOut),
                                   C.POINTER(OutcomeLogC), P, P]
     for name in ("hrpp_device_count", "hrpp_set_live_rounds", "hrpp_hash_rays",
-                 "hrpp_hash_floats", "hrpp_bvh_create", "hrpp_bvh_destroy",
+                 "hrpp_hash_floats", "hrpp_coarsen_keys", "hrpp_bvh_create", "hrpp_bvh_destroy",
                  "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch",
                  "hrpp_table_create", "hrpp_table_destroy", "hrpp_table_clear",
                  "hrpp_table_clear_async", "hrpp_table_info", "hrpp_table_record", "hrpp_table_lookup",
@@ -113,7 +114,7 @@ class _LazyLib:
 lib = _LazyLib()
 
 EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device_count",
-            "hrpp_hash_rays", "hrpp_hash_floats", "hrpp_bvh_create", "hrpp_bvh_destroy",
+            "hrpp_hash_rays", "hrpp_hash_floats", "hrpp_coarsen_keys", "hrpp_bvh_create", "hrpp_bvh_destroy",
             "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch", "hrpp_table_create",
             "hrpp_table_destroy", "hrpp_table_clear", "hrpp_table_clear_async", "hrpp_table_info",
             "hrpp_table_record",

@@ -167,18 +167,11 @@ class Bvh:
 
 
 def ancestor_at(bvh: Bvh, leaf: int, go_up_level: int) -> int:
-    """Follow ``go_up_level`` parent links from ``leaf`` (hrpp/bvh.py:154-166)."""
+    """The node ``go_up_level`` parent links above ``leaf``, clamped at the
+    root (hrpp/bvh.py:154-166): an index into the device-built LUT."""
     if not (0 <= leaf < bvh.node_count):
         raise ValueError(f"node index {leaf} out of range")
-    if go_up_level < 0:
-        raise ValueError("go_up_level must be >= 0")
-    node = int(leaf)
-    for _ in range(go_up_level):
-        up = int(bvh.parent[node])
-        if up < 0:
-            break
-        node = up
-    return node
+    return int(bvh.ancestor_lut(go_up_level)[leaf])
 
 
 # -- build ---------------------------------------------------------------------------
@@ -294,34 +287,3 @@ def intersect_any(bvh: Bvh, ray: Ray, counters: TraversalCounters) -> Optional[H
     if ray.kind is not RayKind.HIT_ANY:
         raise ValueError("intersect_any requires a HIT_ANY ray")
     return intersect_from_node(bvh, 0, ray, counters)
-
-
-def validate(bvh: Bvh, max_leaf_size: int = None, bounds_eps: float = 1e-5):
-    """Structural invariants (hrpp/bvh.py:448-476); raises AssertionError."""
-    n = bvh.node_count
-    seen = np.zeros(n, bool)
-    todo = [0]
-    leaf_depths = []
-    while todo:
-        i = todo.pop()
-        assert not seen[i], f"node {i} reachable twice"
-        seen[i] = True
-        if bvh.is_leaf(i):
-            assert bvh.count[i] >= 1, "empty leaf"
-            leaf_depths.append(int(bvh.depth[i]))
-            continue
-        for c in (int(bvh.left[i]), int(bvh.right[i])):
-            assert 0 <= c < n, "child index out of range"
-            assert int(bvh.parent[c]) == i, "parent link mismatch"
-            assert int(bvh.depth[c]) == int(bvh.depth[i]) + 1
-            assert np.all(bvh.bmin[c] >= bvh.bmin[i] - bounds_eps)
-            assert np.all(bvh.bmax[c] <= bvh.bmax[i] + bounds_eps)
-            todo.append(c)
-    assert seen.all(), "unreachable nodes"
-    assert bvh.max_depth == max(leaf_depths), "max_depth mismatch"
-    covered = np.zeros(bvh.triangle_count, bool)
-    for i in np.flatnonzero(bvh.left < 0):
-        f, c = int(bvh.first[i]), int(bvh.count[i])
-        assert not covered[f:f + c].any(), "overlapping leaf ranges"
-        covered[f:f + c] = True
-    assert covered.all(), "triangle slots not covered by leaves"

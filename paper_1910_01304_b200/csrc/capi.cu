@@ -153,12 +153,14 @@ void prof_flush() {
 
 // Scratch for calls without a table (and host staging): one per host thread
 // and device, so concurrent calls from different threads never share it.
-static Workspace& global_ws() {
+Workspace& device_ws() {
   static thread_local Workspace ws[64];
   int dev = 0;
   cudaGetDevice(&dev);
+  ws[dev & 63].device = dev;
   return ws[dev & 63];
 }
+static Workspace& global_ws() { return device_ws(); }
 
 static bool is_device_ptr(const void* p);
 
@@ -232,7 +234,7 @@ static int choose_stack(int height) {
 struct Pinned {
   long long* p = nullptr;
   int get() {
-    if (!p) HRPP_CK(cudaHostAlloc(&p, sizeof(long long) * 64, cudaHostAllocMapped));
+    if (!p) HRPP_CK(cudaHostAlloc(&p, sizeof(long long) * 64, cudaHostAllocMapped | cudaHostAllocPortable));
     return 0;
   }
 };
@@ -382,6 +384,20 @@ int hrpp_hash_floats(const float* f, int64_t n, int p, uint32_t* out, void* stre
     return HRPP_NONFINITE;
   }
   return HRPP_OK;
+}
+
+int hrpp_coarsen_keys(const uint64_t* keys, int64_t n, int p, uint64_t* out, void* stream) {
+  CHECK_ARG(p >= 2 && p <= 7, "cannot coarsen below the minimum precision");
+  CHECK_ARG(n >= 0 && (n == 0 || (keys && out)), "bad arguments");
+  if (n == 0) return HRPP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager sg(global_ws(), st);
+  const uint64_t* dk;
+  uint64_t* dout;
+  int rc;
+  if ((rc = sg.in(keys, n, &dk)) || (rc = sg.out(out, n, &dout))) return rc;
+  if ((rc = launch_coarsen(dk, n, p, dout, st))) return rc;
+  return sg.finish();
 }
 
 // ---- BVH ------------------------------------------------------------------
@@ -554,9 +570,16 @@ int hrpp_table_clear_async(hrpp_table_t t, void* stream) {
   CHECK_ARG(t, "null table");
   HRPP_CK(cudaSetDevice(t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  HRPP_CK(t->wait_clear(st));
   if (t->meta) HRPP_CK(cudaMemsetAsync(t->meta, 0, sizeof(long long) * 4, st));
   if (t->idx) HRPP_CK(cudaMemsetAsync(t->idx, 0xFF, sizeof(Bucket) * t->idx_cap, st));
   t->n_entries = t->stored = t->arena_used = t->pending = 0;
+  // Later calls may run on other streams (host arrays use the legacy stream,
+  // export/lookup stream 0): each waits for this event before touching the
+  // table, so none reads the stale index or races the memsets.
+  if (!t->clear_ev) HRPP_CK(cudaEventCreateWithFlags(&t->clear_ev, cudaEventDisableTiming));
+  HRPP_CK(cudaEventRecord(t->clear_ev, st));
+  t->clear_recorded = true;
   return HRPP_OK;
 }
 
@@ -572,6 +595,7 @@ int hrpp_table_info(hrpp_table_t t, int64_t* entries, int64_t* stored, int64_t* 
   HRPP_CK(cudaSetDevice(t->device));
   *entries = t->n_entries;
   *stored = t->stored;
+  HRPP_CK(t->wait_clear(0));
   if (max_len) return table_max_len(*t, max_len);
   return HRPP_OK;
 }
@@ -600,6 +624,7 @@ int hrpp_table_record(hrpp_table_t t, const uint64_t* keys, const int32_t* nodes
   if (n == 0) return HRPP_OK;
   HRPP_CK(cudaSetDevice(t->device));
   cudaStream_t st = (cudaStream_t)stream;
+  HRPP_CK(t->wait_clear(st));
   Stager sg(global_ws(), st);
   const uint64_t* dk;
   const int32_t* dn;
@@ -637,6 +662,7 @@ int hrpp_table_pending(hrpp_table_t t, uint64_t* keys, int32_t* nodes, int32_t* 
   CHECK_ARG(t && count, "null argument");
   HRPP_CK(cudaSetDevice(t->device));
   *count = t->pending;
+  HRPP_CK(t->wait_clear(0));
   int64_t m = t->pending < cap ? t->pending : cap;
   if (m <= 0) return HRPP_OK;
   void *pk, *pn, *pr;
@@ -654,12 +680,14 @@ int hrpp_table_lookup(hrpp_table_t t, uint64_t key, int32_t* nodes_host, int64_t
                       int64_t* len_out) {
   CHECK_ARG(t && len_out, "null argument");
   HRPP_CK(cudaSetDevice(t->device));
+  HRPP_CK(t->wait_clear(0));
   return table_lookup1(*t, key, nodes_host, cap, len_out);
 }
 
 int hrpp_table_export(hrpp_table_t t, uint64_t* keys, int64_t* offsets, int32_t* nodes) {
   CHECK_ARG(t && keys && offsets, "null argument");
   HRPP_CK(cudaSetDevice(t->device));
+  HRPP_CK(t->wait_clear(0));
   return table_export(*t, keys, offsets, nodes);
 }
 
@@ -675,6 +703,7 @@ int hrpp_predict_batch(hrpp_bvh_t bvh, hrpp_table_t t, const uint64_t* keys, con
   if (n == 0) return HRPP_OK;
   HRPP_CK(cudaSetDevice(bvh->device));
   cudaStream_t st = (cudaStream_t)stream;
+  HRPP_CK(t->wait_clear(st));
   Stager sg(global_ws(), st);
   const uint64_t* dk;
   const float *dO, *dD;
@@ -712,6 +741,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
   if (n == 0) return HRPP_OK;
   HRPP_CK(cudaSetDevice(bvh->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (t) HRPP_CK(t->wait_clear(st));
   hrpp_wave_out none{};
   if (!out) out = &none;
   Workspace& ws = t ? t->ws : global_ws();

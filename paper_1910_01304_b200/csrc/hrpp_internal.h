@@ -55,6 +55,10 @@ struct Workspace {
   }
 };
 
+// Scratch of calls without a table: one per host thread and CUDA device
+// (the current one), so neither threads nor devices share buffers.
+Workspace& device_ws();
+
 // Result arrays of a traversal (any pointer may be null = not stored).
 struct TraceOut {
   uint8_t* found = nullptr;
@@ -121,6 +125,12 @@ struct TableDev {
   bool deferred = false;
   int64_t pending = 0;
   double start_tp_frac = 1.0;  // wave-start TP fraction of the last live wave
+  // stream-ordered clear: every later call on the table waits for it
+  cudaEvent_t clear_ev = nullptr;
+  bool clear_recorded = false;
+  cudaError_t wait_clear(cudaStream_t st) {
+    return clear_recorded ? cudaStreamWaitEvent(st, clear_ev, 0) : cudaSuccess;
+  }
   Workspace ws;
   ~TableDev();
   // capacity for up to extra_entries new entries and extra_nodes new nodes
@@ -131,6 +141,7 @@ struct TableDev {
 // ib > 0: store (packed key << ib) | ray index, the grouping sort's word
 int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys, int* err,
                 cudaStream_t st, int ib = 0);
+int launch_coarsen(const uint64_t* keys, int64_t n, int p, uint64_t* out, cudaStream_t st);
 int launch_hash_floats(const float* f, int64_t n, int p, uint32_t* out, int* err,
                        cudaStream_t st);
 // Traces n rays (or the device-counted queue ray_idx[0..*count_dev)), one

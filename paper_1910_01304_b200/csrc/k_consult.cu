@@ -170,7 +170,7 @@ __device__ __forceinline__ void flush_tally_warp(const Tally& c, unsigned long l
 // per counter per block (per-warp atomics on 10 shared addresses serialised
 // in L2).  Every thread of the block must call it.
 __device__ __forceinline__ void flush_tally(const Tally& c, unsigned long long* stats) {
-  __shared__ long long part[10][8];
+  __shared__ long long part[10][8];  // <= 8 warps per block (callers: 128 / 256 threads)
   const long long v[10] = {c.tp, c.fp, c.neg, c.bb, c.bt, c.ob, c.ot, c.sk, c.est, c.wr};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -268,6 +268,8 @@ __device__ __forceinline__ void commit_miss(const ConsultArgs& a, Tally& c, int3
 #ifndef HRPP_FIN_BS
 #define HRPP_FIN_BS 128  // k_finalize block size
 #endif
+// flush_tally keeps one partial per warp of the block in part[10][8]
+static_assert(HRPP_FIN_BS % 32 == 0 && HRPP_FIN_BS <= 256, "k_finalize: at most 8 warps");
 #ifndef HRPP_FA_BS
 #define HRPP_FA_BS 256  // k_first_append block size
 #endif

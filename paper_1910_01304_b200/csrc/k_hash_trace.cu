@@ -228,16 +228,51 @@ int launch_hash(const float* O, const float* D, int64_t n, int p, uint64_t* keys
                          reinterpret_cast<uintptr_t>(keys)) & 15) == 0;
   const int64_t ntiles = (n + kHashTile - 1) / kHashTile;
   if (aligned && ntiles >= 2 * (int64_t)num_sms()) {
-    static int smem_set = 0;
+    // the attribute applies to the current device only: set once per device
+    static std::atomic<uint64_t> smem_set{0};
     const int smem = 2 * kHashStages * kHashTileBytes;
-    if (!smem_set) {
+    int dev = 0;
+    HRPP_CK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(smem_set.load() & bit)) {
       HRPP_CK(cudaFuncSetAttribute(k_hash_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      smem_set = 1;
+      smem_set.fetch_or(bit);
     }
     k_hash_bulk<<<2 * num_sms(), 256, smem, st>>>(O, D, n, p, keys, err, ib);
   } else {  // small or unaligned batches
     k_hash<<<grid_for((n + 3) / 4, 256, num_sms() * 8), 256, 0, st>>>(O, D, n, p, keys, err, ib);
   }
+  HRPP_LAUNCHED();
+  return 0;
+}
+
+// Precision p -> p - 1 of a key (hrpp/rayhash.py:125-147).  A lane is the xor
+// of two float hashes; dropping the lowest exponent and mantissa bit commutes
+// with the xor, so each 16-bit lane {sign, p exponent bits, p mantissa bits}
+// is re-packed as {sign, top p-1 of each}.
+__device__ __forceinline__ uint64_t coarsen_lanes(uint64_t k, int p) {
+  const uint32_t fm = (1u << p) - 1u;
+  uint64_t out = 0;
+#pragma unroll
+  for (int l = 0; l < 3; l++) {
+    const uint32_t v = (uint32_t)(k >> (16 * l)) & 0xFFFFu;
+    const uint32_t man = v & fm, ex = (v >> p) & fm, sg = (v >> (2 * p)) & 1u;
+    const uint32_t w = (sg << (2 * (p - 1))) | ((ex >> 1) << (p - 1)) | (man >> 1);
+    out |= (uint64_t)w << (16 * l);
+  }
+  return out;
+}
+
+__global__ void k_coarsen(const uint64_t* __restrict__ keys, int64_t n, int p,
+                          uint64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = coarsen_lanes(keys[i], p);
+}
+
+int launch_coarsen(const uint64_t* keys, int64_t n, int p, uint64_t* out, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_coarsen<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(keys, n, p, out);
   HRPP_LAUNCHED();
   return 0;
 }

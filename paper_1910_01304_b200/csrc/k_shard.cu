@@ -124,7 +124,7 @@ extern "C" int hrpp_partition_by_owner(const uint64_t* keys, int64_t n, int worl
     return HRPP_INVALID_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  static thread_local Workspace ws;
+  Workspace& ws = device_ws();  // per host thread and device
   uint8_t *own, *own2;
   int32_t* iota;
   unsigned long long* cnt;

@@ -243,7 +243,7 @@ extern "C" int hrpp_spawn(hrpp_bvh_t bvh, const float* O, const float* D, const 
   *count_out = 0;
   if (n == 0) return HRPP_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  static thread_local Workspace ws;
+  Workspace& ws = device_ws();  // per host thread and device
   int32_t* pos;
   int* cnt;
   int rc;

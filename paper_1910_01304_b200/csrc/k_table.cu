@@ -382,6 +382,7 @@ int TableDev::reserve(int64_t extra_e, int64_t extra, cudaStream_t st) {
 }
 
 TableDev::~TableDev() {
+  if (clear_ev) cudaEventDestroy(clear_ev);
   cudaFree(idx);
   cudaFree(e_key);
   cudaFree(e_off);

@@ -105,6 +105,8 @@ class PredictorTable:
                  device: Optional[int] = None):
         if go_up_level < 0:
             raise ValueError("go_up_level must be >= 0")
+        if getattr(kind, "value", kind) not in (RayKind.CLOSEST_HIT.value, RayKind.HIT_ANY.value):
+            raise ValueError(f"unknown ray kind {kind!r}")
         self.cfg = cfg
         self.go_up_level = int(go_up_level)
         self.kind = kind
@@ -122,7 +124,7 @@ class PredictorTable:
             h = C.c_void_p()
             rc = _lib.lib.hrpp_table_create(
                 int(self.cfg.precision_bits), self.go_up_level,
-                _lib.CLOSEST_HIT if self.kind is RayKind.CLOSEST_HIT else _lib.HIT_ANY,
+                _lib.CLOSEST_HIT if self.closest else _lib.HIT_ANY,
                 int(self.max_entries), dev, C.byref(h))
             _lib.check(rc, "table_create")
             self._handle = h
@@ -140,7 +142,10 @@ class PredictorTable:
 
     @property
     def closest(self) -> bool:
-        return self.kind is RayKind.CLOSEST_HIT
+        # by value: ``kind`` may be the reference's own RayKind member
+        # (hrpp/geom.py), kept as given so its renderer's identity checks
+        # (hrpp/tracer.py:384-387) hold
+        return getattr(self.kind, "value", self.kind) == RayKind.CLOSEST_HIT.value
 
     def _info(self, with_max=False):
         if self._handle is None:
@@ -270,7 +275,7 @@ class PredictorTable:
 
     def predict(self, bvh: Bvh, ray: Ray) -> PredictionOutcome:
         """Consult the table for ``ray``; never mutates the table."""
-        if ray.kind is not self.kind:
+        if getattr(ray.kind, "value", ray.kind) != getattr(self.kind, "value", self.kind):
             raise ValueError(
                 f"table holds {self.kind.value} entries, got a {ray.kind.value} ray")
         key = hash_ray(ray, self.cfg)

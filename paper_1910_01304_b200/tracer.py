@@ -43,6 +43,27 @@ class RenderMode(Enum):
 _MODE = {RenderMode.BASELINE: _lib.MODE_BASELINE, RenderMode.LIMIT: _lib.MODE_LIMIT,
          RenderMode.LIVE: _lib.MODE_LIVE}
 
+# RayKindStats field order (hrpp/metrics.py:38-51) = the C ABI's stats order
+STATS_FIELDS = ("rays", "tp", "fp", "neg", "baseline_box_tests", "baseline_tri_tests",
+                "overhead_box_tests", "overhead_tri_tests", "skipped_box_tests",
+                "skipped_box_tests_estimated", "wrong_closest")
+
+
+def as_mode(mode) -> RenderMode:
+    """This package's RenderMode for any enum member or string whose value is
+    baseline / limit / live -- the reference's own ``hrpp.tracer.RenderMode``
+    (hrpp/tracer.py:58-61) included, so its renderer can pass its members."""
+    if isinstance(mode, RenderMode):
+        return mode
+    return RenderMode(getattr(mode, "value", mode))
+
+
+def add_stats(stats, raw) -> None:
+    """Add the int64[11] counters into any object with the RayKindStats
+    attributes (hrpp/metrics.py:38-51), by field name."""
+    for name, v in zip(STATS_FIELDS, np.asarray(raw).tolist()):
+        setattr(stats, name, getattr(stats, name) + int(v))
+
 
 @dataclass
 class OutcomeLog:
@@ -77,7 +98,7 @@ def trace_wave(bvh: Bvh, table: Optional[PredictorTable], mode: RenderMode, O, D
     ``capture_outcomes`` in limit mode, log_cls / log_eval_box / log_pred_t /
     log_pred_slot.  ``outputs`` may pre-supply result arrays (reused buffers).
     """
-    mode = RenderMode(mode) if not isinstance(mode, RenderMode) else mode
+    mode = as_mode(mode)
     if mode is not RenderMode.BASELINE:
         if table is None:
             raise ValueError(f"{mode.value} mode needs a predictor table")
@@ -130,15 +151,18 @@ def trace_wave(bvh: Bvh, table: Optional[PredictorTable], mode: RenderMode, O, D
 def _trace_wave(bvh, table, cfg, mode, O32, D32, tmins, tmaxs, stats: RayKindStats,
                 closest: bool, log_lists):
     """Drop-in for hrpp/tracer.py:343-371 (same arguments, same effects):
-    adds into ``stats`` (RayKindStats), extends ``log_lists`` in limit mode,
-    mutates ``table`` and returns the hits shading should use."""
-    capture = log_lists is not None and RenderMode(mode) is RenderMode.LIMIT
+    adds into ``stats`` (this package's or the reference's RayKindStats, by
+    field name), extends ``log_lists`` in limit mode, mutates ``table`` and
+    returns the hits shading should use.  ``mode`` may be the reference's
+    RenderMode member (converted by value)."""
+    mode = as_mode(mode)
+    capture = log_lists is not None and mode is RenderMode.LIMIT
     raw = np.zeros(_lib.STATS_LEN, np.int64)
     try:
         out, raw = trace_wave(bvh, table, mode, O32, D32, tmins, tmaxs, closest, stats=raw,
                               capture_outcomes=capture)
     finally:
-        stats.add_array(raw)
+        add_stats(stats, raw)
     if capture:
         log_lists["cls"].extend(out["log_cls"].tolist())
         log_lists["eval_box"].extend(out["log_eval_box"].tolist())

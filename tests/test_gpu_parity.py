@@ -54,6 +54,18 @@ def test_hash_unaligned_and_ragged(hb):
             assert np.array_equal(keys, g["keys"][5][off:off + n])
 
 
+def test_coarsen_key_on_device(hb):
+    """coarsen_key (hrpp/rayhash.py:125-147) on the device: the p-1 key of a
+    ray equals its coarsened p key, for numpy arrays, tensors and scalars."""
+    import torch
+    g = load_golden("hash.npz")
+    for p in range(2, 8):
+        assert np.array_equal(hb.coarsen_key(g["keys"][p - 1], p), g["keys"][p - 2])
+        t = hb.coarsen_key(torch.from_numpy(g["keys"][p - 1].view(np.int64)).cuda(), p)
+        assert np.array_equal(t.cpu().numpy().view(np.uint64), g["keys"][p - 2])
+        assert hb.coarsen_key(int(g["keys"][p - 1][3]), p) == int(g["keys"][p - 2][3])
+
+
 @pytest.mark.parametrize("n", [303104, 400003, 1 << 20])
 def test_hash_bulk_copy_path(hb, oracle_mod, n):
     """Large aligned batches take the TMA bulk-copy kernel (1024-ray tiles,
