@@ -48,13 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--res", default=None, help="override resolution WxH (testing)")
     ap.add_argument("--spp", type=int, default=None)
     ap.add_argument("--precision", type=int, default=6)
     ap.add_argument("--go-up", type=int, default=0)
-    ap.add_argument("--cpu-sample", type=float, default=0.125,
-                    help="fraction (prefix) of every wave timed on the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
@@ -72,20 +70,24 @@ def parse():
 # workload
 # ---------------------------------------------------------------------------
 
-def make_workload(args, trace_closest=None):
+def make_workload(args, trace_closest=None, build=None):
     """Scene, BVH and the ordered waves of one frame (host numpy).
 
     Waves: the primary wave; shadow rays (one wave per light) from its hits;
     then for every diffuse bounce b = 1..B the bounce wave spawned from the
     previous closest-hit wave, followed by its shadow waves except after the
-    last bounce.  `trace_closest` gives the full-traversal hits used for
-    spawning (GPU in our arm, the oracle in the reference arm; bit-identical).
-    Returns [(name, kind, closest, O, D, tmin, tmax), ...]."""
-    import paper_1910_01304_b200 as hb
-    from paper_1910_01304_b200 import scenes
+    last bounce.  `build` makes the BVH (the native builder in our arm, the
+    oracle's restatement of the reference builder in the reference arm) and
+    `trace_closest` gives the full-traversal hits used for spawning (GPU in
+    our arm, the oracle in the reference arm); both pairs are bit-identical.
+    Returns (scene, bvh, [(name, kind, closest, O, D, tmin, tmax), ...])."""
+    from paper_1910_01304_b200 import scenes  # numpy only: loads no native library
     res = tuple(int(x) for x in args.res.split("x")) if args.res else None
     sc = scenes.make_scene(args.config, resolution=res, spp=args.spp)
-    bvh = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
+    if build is None:
+        import paper_1910_01304_b200 as hb
+        build = hb.build_bvh_from_arrays
+    bvh = build(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
     normals = scenes.slot_normals(bvh.tv0, bvh.tv1, bvh.tv2)
     O, D = scenes.primary_rays(sc.camera, sc.spp, seed=0)
     n = O.shape[0]
@@ -499,28 +501,22 @@ def run_ours(args, rank, world, local_rank):
     # ---- CPU baseline (oracle port, rank 0, N=1 only) ---------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_frame(bvh, waves, args)
+        dt, n_cpu, threads = cpu_reference_frame(_oracle_bvh(bvh), waves, args)
+        cpu = {"value": round(n_cpu / dt / 1e6, 4), "unit": "Mrays/s", "cores": threads,
+               "kind": "port", "sample": cpu_sample_desc(n_cpu, threads),
+               "seconds": round(dt, 3)}
 
     if rank == 0:
-        res = sc.camera.resolution
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_live / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded displaced icosphere scene + generated ray waves)",
-            "config": {"workload": f"{args.config}: {sc.n_tris} tris, {res[0]}x{res[1]} spp"
-                                   f"{sc.spp}, {len(waves)} waves ("
-                                   + ", ".join(w[0] for w in waves) + ")",
-                       "mode": "live (predict, else full traversal, train in ray order)",
-                       "rays_per_step": n_total,
-                       "rays_per_wave": {w[0]: int(w[3].shape[0]) for w in waves},
-                       "bvh_nodes": bvh.node_count, "bvh_max_depth": bvh.max_depth,
-                       "precision": args.precision, "go_up": args.go_up,
-                       "parallelism": (f"key sharding x{world} (exact; all-to-all of rays "
-                                       "to key owners)" if keyed else
-                                       f"contiguous ray blocks x{world}"),
-                       "l2": "inputs > L2 (335 MB primary wave); no flush needed"},
+            "config": dict(workload_config(args, sc, bvh, waves),
+                           parallelism=(f"key sharding x{world} (exact; all-to-all of rays "
+                                        "to key owners)" if keyed else
+                                        f"contiguous ray blocks x{world}")),
             "full_traversal_mrays_s": round(base_value, 3),
             "speedup_vs_full_traversal": round(value / base_value, 4),
             "nodes_skipped_percent": savings,
@@ -548,6 +544,19 @@ def run_ours(args, rank, world, local_rank):
 # CPU reference (the oracle port; reference arm and cpu_baseline)
 # ---------------------------------------------------------------------------
 
+def workload_config(args, sc, bvh, waves):
+    """The line's `config`, identical in both arms (same scene, BVH, waves)."""
+    res = sc.camera.resolution
+    return {"workload": f"{args.config}: {sc.n_tris} tris, {res[0]}x{res[1]} spp{sc.spp}, "
+                        f"{len(waves)} waves (" + ", ".join(w[0] for w in waves) + ")",
+            "mode": "live (predict, else full traversal, train in ray order)",
+            "rays_per_step": int(sum(w[3].shape[0] for w in waves)),
+            "rays_per_wave": {w[0]: int(w[3].shape[0]) for w in waves},
+            "bvh_nodes": int(bvh.node_count), "bvh_max_depth": int(bvh.max_depth),
+            "precision": args.precision, "go_up": args.go_up,
+            "l2": "inputs > L2 (335 MB primary wave); no flush needed"}
+
+
 def _oracle_bvh(bvh):
     from oracle import oracle
     oracle.build()
@@ -556,60 +565,62 @@ def _oracle_bvh(bvh):
                             bvh.tri_ids)
 
 
-def cpu_reference_frame(bvh, waves, args, steps=1):
-    """Live-mode frame on a contiguous prefix sample of every wave through the
-    oracle (hrpp/tracer.py:278-340 restated in C).  The reference's live
-    consult is single-threaded by design (hrpp/tracer.py:12-15), so is this."""
+def cpu_reference_frame(ob, waves, args):
+    """One live-mode frame (every ray of every wave, fresh tables) through the
+    oracle: the reference's sequential consult loop (hrpp/tracer.py:278-340
+    restated in C) on every host core, each core running it for the keys it
+    owns (exact: a key's entry is read and written only by its own rays).
+    Returns (seconds, rays, threads)."""
     from oracle import oracle
-    ob = _oracle_bvh(bvh)
-    frac = args.cpu_sample
-    sample = [(w[2], *(a[:max(1, int(len(a) * frac))] for a in w[3:])) for w in waves]
-    n = sum(s_[1].shape[0] for s_ in sample)
-    best = None
-    for _ in range(steps):
-        tabs = {c: oracle.OracleTable(args.precision, args.go_up, c) for c in (True, False)}
-        t0 = time.perf_counter()
-        for closest, O, D, a, b in sample:
-            rc, _, _ = oracle.trace_wave(ob, tabs[closest], "live", closest, O, D, a, b, threads=1)
-            assert rc == 0
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return {"value": round(n / best / 1e6, 4), "unit": "Mrays/s", "cores": 1, "kind": "port",
-            "sample": f"first {frac:g} of every wave of one frame ({n} rays), live mode, "
-                      f"fresh tables; C oracle (oracle/hrpp_oracle.c), 1 thread (the "
-                      f"reference's consult loop is sequential); host has {os.cpu_count()} "
-                      f"cores",
-            "seconds": round(best, 3)}
+    threads = os.cpu_count() or 1
+    tabs = {c: oracle.ShardedTable(args.precision, args.go_up, c, shards=threads)
+            for c in (True, False)}
+    n = 0
+    t0 = time.perf_counter()
+    for _, _, closest, O, D, a, b in waves:
+        rc, _, _ = oracle.trace_wave(ob, tabs[closest], "live", closest, O, D, a, b)
+        assert rc == 0
+        n += O.shape[0]
+    return time.perf_counter() - t0, n, threads
+
+
+def cpu_sample_desc(n, threads):
+    return (f"one full live-mode frame ({n} rays, every wave, fresh tables); C oracle "
+            f"(oracle/hrpp_oracle.c, the reference's consult loop restated) on {threads} host "
+            f"threads, keys sharded across threads (exact); host has {os.cpu_count()} cores")
 
 
 def run_reference(args, rank, world):
+    """The reference algorithm on the host cores for the same frame: scene
+    and waves from the same generators, the BVH from the oracle's own
+    restatement of the reference builder, full-traversal spawning and the
+    timed frames through the oracle.  Never loads the product library."""
     if rank != 0:
         return
+    from oracle import oracle
+    oracle.build()
 
-    def cpu_trace(bvh, O, D, t0, t1):
-        return _oracle_bvh(bvh).trace_batch(True, O, D, t0, t1, threads=0)
+    def cpu_trace(b, O, D, t0, t1):
+        return b.trace_batch(True, O, D, t0, t1, threads=0)
 
-    sc, bvh, waves = make_workload(args, cpu_trace)
-    for _ in range(min(args.warmup, 1)):
-        cpu_reference_frame(bvh, waves, args)
-    t0 = time.perf_counter()
-    vals = []
-    r = None
+    sc, ob, waves = make_workload(args, cpu_trace, build=oracle.build_bvh)
+    frames = []
+    for _ in range(args.warmup):
+        cpu_reference_frame(ob, waves, args)
     for _ in range(args.steps):
-        r = cpu_reference_frame(bvh, waves, args)
-        vals.append(r["value"])
-    dt = time.perf_counter() - t0
-    value = statistics.median(vals)
+        dt, n, threads = cpu_reference_frame(ob, waves, args)
+        frames.append(dt)
+    total = sum(frames)
+    value = round(n * len(frames) / total / 1e6, 4)
     line = {"metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1000 * dt / args.steps, 3), "higher_is_better": True,
+            "ms_per_step": round(1000 * total / len(frames), 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same seeded scene and waves as our arm)", "impl": "reference",
-            "config": {"workload": f"{args.config}: {sc.n_tris} tris, prefix sample "
-                                   f"{args.cpu_sample:g} of each of {len(waves)} waves",
-                       "mode": "live"},
-            "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": 1, "kind": "port",
-                             "sample": r["sample"]},
+            "config": dict(workload_config(args, sc, ob, waves),
+                           parallelism=f"host threads x{threads}"),
+            "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads,
+                             "kind": "port", "sample": cpu_sample_desc(n, threads)},
             "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -390,15 +390,18 @@ void or_table_export(const or_table *t, uint64_t *keys, int64_t *offsets, int32_
 /* stats layout = RayKindStats field order (hrpp/metrics.py:38-51) */
 enum { S_RAYS, S_TP, S_FP, S_NEG, S_BB, S_BT, S_OB, S_OT, S_SK, S_EST, S_WRONG, S_N };
 
-/* hrpp/tracer.py:217-275.  log_* may be NULL. */
+/* hrpp/tracer.py:217-275.  log_* may be NULL.  With owner != NULL only the
+ * rays whose owner[i] == me are consulted (in ray order): the key-sharded
+ * multi-threaded wave below gives each thread the keys it owns. */
 static int consult_limit(or_table *t, const or_bvh *b, int closest, const uint64_t *keys,
                          const float *O, const float *D, const double *tmins,
                          const double *tmaxs, const uint8_t *bfound, const double *bt,
                          const int32_t *bleaf, const int64_t *bbox, int64_t n, int64_t *stats,
                          int8_t *log_cls, int64_t *log_eval_box, double *log_pred_t,
-                         int64_t *log_pred_slot) {
+                         int64_t *log_pred_slot, const uint16_t *owner, uint16_t me) {
     int64_t tp = 0, fp = 0, neg = 0, ob = 0, ot = 0, sk = 0, est = 0, wrong = 0;
     for (int64_t i = 0; i < n; i++) {
+        if (owner && owner[i] != me) continue;
         uint64_t key = keys[i];
         int64_t e = t_lookup(t, key);
         if (e < 0) {
@@ -439,12 +442,14 @@ static int consult_limit(or_table *t, const or_bvh *b, int closest, const uint64
 static int consult_live(or_table *t, const or_bvh *b, int closest, const uint64_t *keys,
                         const float *O, const float *D, const double *tmins, const double *tmaxs,
                         int64_t n, int64_t *stats, uint8_t *ofound, double *ot_, int32_t *oslot,
-                        int32_t *oleaf) {
+                        int32_t *oleaf, const uint16_t *owner, uint16_t me) {
     int64_t tp = 0, fp = 0, neg = 0, ob = 0, ot = 0, est = 0, bb = 0, bt = 0;
     for (int64_t i = 0; i < n; i++) {
+        if (owner && owner[i] != me) continue;
         ofound[i] = 0; ot_[i] = 0.0; oslot[i] = -1; oleaf[i] = -1;
     }
     for (int64_t i = 0; i < n; i++) {
+        if (owner && owner[i] != me) continue;
         uint64_t key = keys[i];
         int64_t e = t_lookup(t, key);
         int predicted = 0;
@@ -503,7 +508,7 @@ int or_trace_wave(BVH_ARGS, const int32_t *anc, or_table *table, int p, int mode
     }
     if (mode == 2) {
         rc = consult_live(table, &bv, closest, keys, O, D, tmins, tmaxs, n, stats, found, t, slot,
-                          leaf);
+                          leaf, NULL, 0);
         goto done;
     }
     {
@@ -518,13 +523,79 @@ int or_trace_wave(BVH_ARGS, const int32_t *anc, or_table *table, int p, int mode
         stats[S_BB] += sb; stats[S_BT] += st;
         if (mode == 1)
             rc = consult_limit(table, &bv, closest, keys, O, D, tmins, tmaxs, found, t, leaf, bx, n,
-                               stats, log_cls, log_eval_box, log_pred_t, log_pred_slot);
+                               stats, log_cls, log_eval_box, log_pred_t, log_pred_slot, NULL, 0);
         if (!box) free(bx);
         if (!tri) free(tr);
         if (!vis) free(vs);
     }
 done:
     if (keys && keys != keys_out) free(keys);
+    return rc;
+}
+
+/* The same wave with the consult spread over `shards` host threads by key:
+ * thread s owns the keys with (mix64(key) >> 32) % shards == s and runs the
+ * reference's sequential loop over its rays, in ray order, against its own
+ * table tables[s].  A key's entry is read and written only by rays with
+ * that key (hrpp/tracer.py:233-267, :295-331), so hits and statistics are
+ * those of one table and the union of the shards' tables is that table
+ * (the entry cap applies per shard).  Used as the CPU baseline: the
+ * reference's consult is single-threaded by design; this is its result
+ * computed with all host cores. */
+int or_trace_wave_sharded(BVH_ARGS, const int32_t *anc, or_table **tables, int shards, int p,
+                          int mode, int closest, const float *O, const float *D,
+                          const double *tmins, const double *tmaxs, int64_t n, uint8_t *found,
+                          double *t, int32_t *slot, int32_t *leaf, double *u, double *v,
+                          int64_t *box, int64_t *tri, int64_t *vis, uint64_t *keys_out,
+                          int64_t *stats) {
+    if (mode == 0 || shards < 1 || shards > 65535) return OR_INVALID;
+    BVH_INIT(bv);
+    bv.anc = anc;
+    stats[S_RAYS] += n;
+    const int64_t nn = n > 0 ? n : 1;
+    uint64_t *keys = keys_out ? keys_out : (uint64_t *)malloc(sizeof(uint64_t) * nn);
+    uint16_t *owner = (uint16_t *)malloc(sizeof(uint16_t) * nn);
+    int64_t *bx = NULL, *tr = NULL, *vs = NULL;
+    int rc = or_hash_rays(O, D, n, p, keys);
+    if (rc != OR_OK) goto done;
+    for (int64_t i = 0; i < n; i++) owner[i] = (uint16_t)((mix64(keys[i]) >> 32) % (uint64_t)shards);
+    if (mode == 1) {
+        bx = box ? box : (int64_t *)malloc(sizeof(int64_t) * nn);
+        tr = tri ? tri : (int64_t *)malloc(sizeof(int64_t) * nn);
+        vs = vis ? vis : (int64_t *)malloc(sizeof(int64_t) * nn);
+        or_trace_batch(bmin, bmax, left, right, axis, first, count, tv0, tv1, tv2, depth, n_nodes,
+                       n_tris, closest, O, D, tmins, tmaxs, 0, n, found, t, slot, leaf,
+                       closest ? u : NULL, closest ? v : NULL, bx, tr, vs, shards);
+        int64_t sb = 0, st = 0;
+        for (int64_t i = 0; i < n; i++) { sb += bx[i]; st += tr[i]; }
+        stats[S_BB] += sb; stats[S_BT] += st;
+    }
+    int64_t *part = (int64_t *)calloc((size_t)shards * S_N, sizeof(int64_t));
+    int *rcs = (int *)calloc((size_t)shards, sizeof(int));
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1) num_threads(shards)
+#endif
+    for (int s = 0; s < shards; s++) {
+        if (mode == 2)
+            rcs[s] = consult_live(tables[s], &bv, closest, keys, O, D, tmins, tmaxs, n,
+                                  part + (size_t)s * S_N, found, t, slot, leaf, owner, (uint16_t)s);
+        else
+            rcs[s] = consult_limit(tables[s], &bv, closest, keys, O, D, tmins, tmaxs, found, t,
+                                   leaf, bx, n, part + (size_t)s * S_N, NULL, NULL, NULL, NULL,
+                                   owner, (uint16_t)s);
+    }
+    for (int s = 0; s < shards; s++) {
+        for (int k = 1; k < S_N; k++) stats[k] += part[(size_t)s * S_N + k];
+        if (rcs[s] != OR_OK) rc = rcs[s];
+    }
+    free(part);
+    free(rcs);
+done:
+    if (bx && bx != box) free(bx);
+    if (tr && tr != tri) free(tr);
+    if (vs && vs != vis) free(vs);
+    if (keys != keys_out) free(keys);
+    free(owner);
     return rc;
 }
 

@@ -46,14 +46,18 @@ class OracleError(RuntimeError):
         super().__init__(f"oracle {what} failed with status {code}")
 
 
+SOURCES = ("hrpp_oracle.c", "hrpp_oracle_bvh.c")
+
+
 def build(force: bool = False) -> Path:
     """Compile the C oracle with gcc (OpenMP if available)."""
-    src = HERE / "hrpp_oracle.c"
-    if LIB_PATH.exists() and not force and LIB_PATH.stat().st_mtime >= src.stat().st_mtime:
+    srcs = [HERE / s for s in SOURCES]
+    if LIB_PATH.exists() and not force and all(LIB_PATH.stat().st_mtime >= s.stat().st_mtime
+                                               for s in srcs):
         return LIB_PATH
     LIB_PATH.parent.mkdir(parents=True, exist_ok=True)
     base = ["gcc", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-            "-shared", "-o", str(LIB_PATH), str(src), "-lm"]
+            "-shared", "-o", str(LIB_PATH), *map(str, srcs), "-lm"]
     try:
         subprocess.run(base[:1] + ["-fopenmp"] + base[1:], check=True, capture_output=True)
     except subprocess.CalledProcessError:
@@ -69,6 +73,10 @@ def lib():
     if _lib is None:
         if not LIB_PATH.exists():
             build()
+        # idle OpenMP workers sleep instead of spinning: the sharded consult
+        # and the traversal batches alternate with serial work (measured: a
+        # spinning team slowed small sharded waves ~40x)
+        os.environ.setdefault("OMP_WAIT_POLICY", "passive")
         _lib = C.CDLL(str(LIB_PATH))
         _declare(_lib)
     return _lib
@@ -104,6 +112,11 @@ def _declare(L):
     L.or_predict_batch.restype = C.c_int
     L.or_max_threads.argtypes = []
     L.or_max_threads.restype = C.c_int
+    L.or_trace_wave_sharded.argtypes = (bvh + [P, P, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
+                                               P, P, I64] + [P] * 9 + [P, P])
+    L.or_trace_wave_sharded.restype = C.c_int
+    L.or_build_bvh.argtypes = [P, P, P, P, I64, C.c_int, C.c_int] + [P] * 13 + [P, P, P]
+    L.or_build_bvh.restype = C.c_int
 
 
 def _p(a):
@@ -240,6 +253,36 @@ class OracleBvh:
         return out
 
 
+def build_bvh(v0, v1, v2, ids=None, max_leaf_size=4, median_split=False):
+    """hrpp/bvh.py:184-357 restated in C (oracle/hrpp_oracle_bvh.c): the
+    reference builder's arrays, as an OracleBvh (+ ``max_depth``).  Raises
+    ValueError when no triangle survives the degenerate filter."""
+    v0, v1, v2 = (_c(a, np.float32).reshape(-1, 3) for a in (v0, v1, v2))
+    m = v0.shape[0]
+    ids = None if ids is None else _c(ids, np.int32)
+    cap = max(2 * m, 1)
+    o = {k: np.zeros((cap, 3), np.float32) for k in ("bmin", "bmax")}
+    o.update({k: np.zeros(cap, np.int32) for k in ("left", "right", "first", "count", "parent",
+                                                    "depth")})
+    o["axis"] = np.zeros(cap, np.int8)
+    o.update({k: np.zeros((max(m, 1), 3), np.float32) for k in ("tv0", "tv1", "tv2")})
+    o["tri_ids"] = np.zeros(max(m, 1), np.int32)
+    nn, nt, md = I64(), I64(), I32()
+    order = ("bmin", "bmax", "left", "right", "axis", "first", "count", "parent", "depth", "tv0",
+             "tv1", "tv2", "tri_ids")
+    rc = lib().or_build_bvh(_p(v0), _p(v1), _p(v2), _p(ids), m, int(max_leaf_size),
+                            int(bool(median_split)), *(_p(o[k]) for k in order), C.byref(nn),
+                            C.byref(nt), C.byref(md))
+    if rc == INVALID:
+        raise ValueError("no valid triangles remain after filtering")
+    if rc != OK:
+        raise OracleError(rc, "build_bvh")
+    n, t = nn.value, nt.value
+    b = OracleBvh(*(o[k][:n] for k in order[:9]), *(o[k][:t] for k in order[9:]))
+    b.max_depth = md.value
+    return b
+
+
 # --------------------------------------------------------------------------
 # predictor table + wave
 # --------------------------------------------------------------------------
@@ -292,6 +335,42 @@ class OracleTable:
                 + "]" for i, k in enumerate(keys)]
 
 
+class ShardedTable:
+    """One logical predictor table held as ``shards`` key-disjoint tables,
+    one per host thread (see or_trace_wave_sharded): trace_wave consults
+    each shard's keys on its own thread, in ray order.  export() and
+    dump_lines() give the union, sorted by key -- the single table's."""
+
+    def __init__(self, p=6, go_up_level=0, closest=True, shards=None, max_entries=1 << 26):
+        self.p = int(p)
+        self.go_up_level = int(go_up_level)
+        self.closest = bool(closest)
+        self.shards = [OracleTable(p, go_up_level, closest, max_entries)
+                       for _ in range(int(shards or os.cpu_count() or 1))]
+        self._arr = (C.c_void_p * len(self.shards))(*(s._h for s in self.shards))
+
+    def info(self):
+        e = [s.info() for s in self.shards]
+        return sum(x[0] for x in e), sum(x[1] for x in e), max(x[2] for x in e)
+
+    def export(self):
+        parts = [s.export() for s in self.shards]
+        keys = np.concatenate([k for k, _, _ in parts])
+        lists = [nd[o[i]:o[i + 1]] for _, o, nd in parts for i in range(len(o) - 1)]
+        order = np.argsort(keys, kind="stable")
+        lens = np.array([len(lists[i]) for i in order], np.int64)
+        offs = np.zeros(len(order) + 1, np.int64)
+        np.cumsum(lens, out=offs[1:])
+        nodes = (np.concatenate([lists[i] for i in order]) if len(order)
+                 else np.zeros(0, np.int32))
+        return keys[order], offs, nodes.astype(np.int32)
+
+    def dump_lines(self):
+        keys, offs, nodes = self.export()
+        return [f"{int(k):012x} -> [" + ",".join(str(int(x)) for x in nodes[offs[i]:offs[i + 1]])
+                + "]" for i, k in enumerate(keys)]
+
+
 MODES = {"baseline": 0, "limit": 1, "live": 2}
 
 
@@ -317,6 +396,16 @@ def trace_wave(bvh: OracleBvh, table, mode, closest, O, D, tmins, tmaxs, stats=N
         log = {"cls": np.zeros(n, np.int8), "eval_box": np.zeros(n, np.int64),
                "pred_t": np.zeros(n), "pred_slot": np.zeros(n, np.int64)}
     anc = bvh.ancestor_lut(table.go_up_level) if table is not None else None
+    if isinstance(table, ShardedTable) and m != 0:
+        rc = lib().or_trace_wave_sharded(
+            *bvh._args(), _p(anc), table._arr, len(table.shards), table.p, m,
+            int(bool(closest)), _p(O), _p(D), _p(_c(tmins, np.float64)),
+            _p(_c(tmaxs, np.float64)), n, _p(out["found"]), _p(out["t"]), _p(out["slot"]),
+            _p(out["leaf"]), _p(out.get("u")), _p(out.get("v")), _p(out.get("box")),
+            _p(out.get("tri")), _p(out.get("visited")), _p(keys), _p(stats))
+        if keys is not None:
+            out["keys"] = keys
+        return rc, out, stats
     rc = lib().or_trace_wave(
         *bvh._args(), _p(anc), None if table is None else table._h,
         0 if table is None else table.p, m, int(bool(closest)), _p(O), _p(D),

@@ -130,3 +130,72 @@ def test_capacity(oracle_mod):
     assert rc == 0
     rc, _ = t.record_batch(np.array([3], np.uint64), np.array([0], np.int32))
     assert rc == oracle_mod.CAPACITY
+
+
+def _tris_from_bvh(g):
+    order = np.argsort(g["tri_ids"], kind="stable")
+    return g["tv0"][order], g["tv1"][order], g["tv2"][order], g["tri_ids"][order]
+
+
+@pytest.mark.parametrize("name,leaf", [("strip8", 1), ("soup256", 4), ("spheres", 4),
+                                       ("ico1282", 4)])
+def test_oracle_builder_matches_reference(oracle_mod, name, leaf):
+    """The oracle's C restatement of the SAH builder (hrpp/bvh.py:184-357)
+    reproduces the reference-built golden BVHs array for array."""
+    g = load_golden(f"bvh_{name}.npz")
+    if "in_v0" in g:
+        v0, v1, v2, ids = g["in_v0"], g["in_v1"], g["in_v2"], None
+    else:
+        v0, v1, v2, ids = _tris_from_bvh(g)
+    b = oracle_mod.build_bvh(v0, v1, v2, ids=ids, max_leaf_size=leaf)
+    for k in ("bmin", "bmax", "left", "right", "axis", "first", "count", "parent", "depth",
+              "tv0", "tv1", "tv2", "tri_ids"):
+        assert np.array_equal(getattr(b, k), g[k]), k
+    assert b.max_depth == int(g["max_depth"])
+
+
+def test_oracle_builder_edge_cases(oracle_mod):
+    with pytest.raises(ValueError):  # every triangle degenerate (bvh.py:195-201)
+        oracle_mod.build_bvh(np.zeros((2, 3)), np.ones((2, 3)), 2 * np.ones((2, 3)))
+    t = np.array([[0, 0, 0]], np.float32), np.array([[1, 0, 0]], np.float32), \
+        np.array([[0, 1, 0]], np.float32)
+    b = oracle_mod.build_bvh(*(np.repeat(a, 3, axis=0) for a in t), max_leaf_size=1)
+    assert b.node_count == 1 and int(b.count[0]) == 3  # coincident centroids: one leaf
+
+
+@pytest.mark.parametrize("median", [False, True])
+def test_oracle_builder_matches_native_builder(oracle_mod, median):
+    """Same arrays as the product's native builder on a BASELINE c1 scene
+    (the median-split option has no reference counterpart: both builders
+    implement the reference's forced split at every oversized node)."""
+    import paper_1910_01304_b200 as hb
+    from paper_1910_01304_b200.scenes import make_scene
+    sc = make_scene("c1")
+    a = oracle_mod.build_bvh(sc.v0, sc.v1, sc.v2, median_split=median)
+    b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=median)
+    for k in ("bmin", "bmax", "left", "right", "axis", "first", "count", "parent", "depth",
+              "tv0", "tv1", "tv2", "tri_ids"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    assert a.max_depth == b.max_depth
+
+
+@pytest.mark.parametrize("p,g_", ((6, 0), (3, 0), (4, 2)))
+@pytest.mark.parametrize("mode", ["limit", "live"])
+@pytest.mark.parametrize("shards", [2, 5])
+def test_sharded_oracle_equals_reference(oracle_mod, p, g_, mode, shards):
+    """The key-sharded multi-threaded consult (the CPU baseline's) gives the
+    reference's hits, statistics and table (union of the shards)."""
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden(f"wave_{mode}_p{p}_g{g_}.npz")
+    b = obvh(oracle_mod, "spheres")
+    tables = {c: oracle_mod.ShardedTable(p, g_, c, shards=shards) for c in (True, False)}
+    for w in WAVES:
+        closest = w != "shadow"
+        rc, out, stats = oracle_mod.trace_wave(b, tables[closest], mode, closest, inp[f"{w}_O"],
+                                               inp[f"{w}_D"], inp[f"{w}_tmin"],
+                                               inp[f"{w}_tmax"])
+        assert rc == 0
+        assert np.array_equal(stats, ref[f"{w}_stats"]), (w, stats, ref[f"{w}_stats"])
+        for k in ("found", "t", "slot", "leaf"):
+            assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
+        assert tables[closest].dump_lines() == list(ref[f"{w}_dump"])
