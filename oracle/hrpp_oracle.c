@@ -486,7 +486,148 @@ static int consult_live(or_table *t, const or_bvh *b, int closest, const uint64_
     return OR_OK;
 }
 
-/* hrpp/tracer.py:343-371.  mode: 0 baseline, 1 limit, 2 live.
+/* Fast mode (mode 3): the product's sort-free live mode (DESIGN.md "Fast
+ * mode"), restated sequentially so the GPU can be checked bit for bit.  It
+ * runs the reference's live loop (hrpp/tracer.py:295-331) as rounds of
+ * key-parallel speculation instead of one ray at a time:
+ *  round 0  every ray evaluates its entry as it stood at the start of the
+ *           wave; a hit is a TP (final);
+ *  round k  (1 <= k <= R) among the rays still unresolved, the first of each
+ *           key in ray order is the key's round-k leader: NEG (no entry at
+ *           its turn) or FP, traced from the root (final).  If it hit and
+ *           its node anc[leaf] is new to the entry, every later unresolved
+ *           ray of the key evaluates that node: a hit makes it a TP;
+ *  final    the rays still unresolved after R rounds are traced (NEG or FP).
+ * Records (key, anc[leaf]) of every traced ray with a hit are applied after
+ * the wave in ray order with set semantics (hrpp/predictor.py:147-160).
+ * Every ray's decision sees exactly the nodes earlier rays appended, as in
+ * the reference, EXCEPT the rays resolved in the final pass, which do not see
+ * each other's appends: with R at least the number of appends any key needs
+ * in the wave the statistics, hits and table are the reference's; with
+ * fewer rounds some of those rays are traced instead of predicted (fewer
+ * TPs; DESIGN.md states the measured tolerance).  Counters: overhead = every
+ * entry/node evaluation, baseline = the traced rays' traversals, est over
+ * TPs with the ray's total evaluation boxes. */
+static int g_fast_rounds = 4;
+void or_set_fast_rounds(int r) { g_fast_rounds = r < 0 ? 0 : r; }
+
+typedef struct { int64_t cap; int64_t *ray; } key_map;   /* key -> ray (first/last seen) */
+
+static int64_t *km_slot(key_map *m, const uint64_t *keys, uint64_t key) {
+    uint64_t h = mix64(key) & (uint64_t)(m->cap - 1);
+    while (m->ray[h] >= 0 && keys[m->ray[h]] != key) h = (h + 1) & (uint64_t)(m->cap - 1);
+    return &m->ray[h];
+}
+
+static int fast_wave(or_table *t, const or_bvh *b, int closest, const uint64_t *keys,
+                     const float *O, const float *D, const double *tmins, const double *tmaxs,
+                     int64_t n, int64_t *stats, uint8_t *ofound, double *ot_, int32_t *oslot,
+                     int32_t *oleaf) {
+    int64_t tp = 0, fp = 0, neg = 0, ob = 0, ovt = 0, est = 0, bb = 0, bt = 0;
+    const int64_t nn = n > 0 ? n : 1;
+    int64_t *eid = (int64_t *)malloc(sizeof(int64_t) * nn);
+    int64_t *evbox = (int64_t *)malloc(sizeof(int64_t) * nn);  /* evaluation boxes so far */
+    uint8_t *traced = (uint8_t *)calloc(nn, 1);
+    int64_t *unres = (int64_t *)malloc(sizeof(int64_t) * nn), nu = 0;
+    key_map lead = {1024, NULL}, hit = {1024, NULL}, added = {1024, NULL};
+    while (lead.cap < 2 * nn) lead.cap <<= 1;
+    hit.cap = added.cap = lead.cap;
+    lead.ray = (int64_t *)malloc(sizeof(int64_t) * lead.cap);
+    hit.ray = (int64_t *)malloc(sizeof(int64_t) * lead.cap);    /* key's traced rays hit */
+    for (int64_t h = 0; h < lead.cap; h++) hit.ray[h] = -1;
+    /* appended nodes per key so far: a linked list through `nxt` by ray */
+    int64_t *nxt = (int64_t *)malloc(sizeof(int64_t) * nn);
+    added.ray = (int64_t *)malloc(sizeof(int64_t) * lead.cap);  /* head: last appending ray */
+    for (int64_t h = 0; h < lead.cap; h++) added.ray[h] = -1;
+    /* round 0 */
+    for (int64_t i = 0; i < n; i++) {
+        ofound[i] = 0; ot_[i] = 0.0; oslot[i] = -1; oleaf[i] = -1;
+        eid[i] = t_lookup(t, keys[i]);
+        evbox[i] = 0;
+        if (eid[i] >= 0) {
+            const or_entry *en = &t->entries[eid[i]];
+            or_hit r = eval_entry(b, closest, en->nodes, en->len, O[3 * i], O[3 * i + 1],
+                                  O[3 * i + 2], D[3 * i], D[3 * i + 1], D[3 * i + 2], tmins[i],
+                                  tmaxs[i]);
+            ob += r.boxes; ovt += r.tris;
+            evbox[i] = r.boxes;
+            if (r.found) {
+                tp++;
+                int64_t x = (int64_t)b->depth[r.leaf] + 1 - r.boxes;
+                est += x > 0 ? x : 0;
+                ofound[i] = 1; ot_[i] = r.t; oslot[i] = (int32_t)r.slot; oleaf[i] = (int32_t)r.leaf;
+                continue;
+            }
+        }
+        unres[nu++] = i;
+    }
+    for (int round = 0; round <= g_fast_rounds && nu > 0; round++) {
+        const int last = round == g_fast_rounds;
+        for (int64_t h = 0; h < lead.cap; h++) lead.ray[h] = -1;
+        int64_t keep = 0;
+        for (int64_t u = 0; u < nu; u++) {
+            const int64_t i = unres[u];
+            int64_t *ls = km_slot(&lead, keys, keys[i]);
+            const int is_leader = last || *ls < 0;
+            if (*ls < 0) *ls = i;
+            const double ox = O[3 * i], oy = O[3 * i + 1], oz = O[3 * i + 2];
+            const double dx = D[3 * i], dy = D[3 * i + 1], dz = D[3 * i + 2];
+            int64_t *hs = km_slot(&hit, keys, keys[i]);
+            if (is_leader) {   /* traced: its entry exists iff listed or an earlier trace hit */
+                if (eid[i] >= 0 || *hs >= 0) fp++;
+                else neg++;
+                or_hit h = trace_one(b, closest, ox, oy, oz, dx, dy, dz, tmins[i], tmaxs[i], 0);
+                bb += h.boxes; bt += h.tris;
+                traced[i] = 1;
+                if (h.found) {
+                    ofound[i] = 1; ot_[i] = h.t; oslot[i] = (int32_t)h.slot; oleaf[i] = (int32_t)h.leaf;
+                    if (*hs < 0) *hs = i;
+                    /* a node new to the entry becomes visible to later rays */
+                    const int32_t node = b->anc[h.leaf];
+                    int listed = 0;
+                    if (eid[i] >= 0) {
+                        const or_entry *en = &t->entries[eid[i]];
+                        for (int64_t k = 0; k < en->len && !listed; k++) listed = en->nodes[k] == node;
+                    }
+                    int64_t *as = km_slot(&added, keys, keys[i]);
+                    for (int64_t r = *as; r >= 0 && !listed; r = nxt[r])
+                        listed = b->anc[oleaf[r]] == node;
+                    if (!listed) { nxt[i] = *as; *as = i; }
+                }
+                continue;
+            }
+            /* follower of this round's leader L: L's node, if L appended one */
+            const int64_t L = *ls;
+            int64_t *as = km_slot(&added, keys, keys[i]);
+            if (*as == L) {
+                const int32_t node = b->anc[oleaf[L]];
+                or_hit r = trace_one(b, closest, ox, oy, oz, dx, dy, dz, tmins[i], tmaxs[i], node);
+                ob += r.boxes; ovt += r.tris;
+                evbox[i] += r.boxes;
+                if (r.found) {
+                    tp++;
+                    int64_t x = (int64_t)b->depth[r.leaf] + 1 - evbox[i];
+                    est += x > 0 ? x : 0;
+                    ofound[i] = 1; ot_[i] = r.t; oslot[i] = (int32_t)r.slot; oleaf[i] = (int32_t)r.leaf;
+                    continue;
+                }
+            }
+            unres[keep++] = i;
+        }
+        nu = keep;
+    }
+    int rc = OR_OK;
+    for (int64_t i = 0; i < n && rc == OR_OK; i++)
+        if (traced[i] && ofound[i] && t_record(t, keys[i], b->anc[oleaf[i]]) < 0) rc = OR_CAPACITY;
+    free(eid); free(evbox); free(traced); free(unres); free(lead.ray); free(hit.ray);
+    free(added.ray); free(nxt);
+    stats[S_TP] += tp; stats[S_FP] += fp; stats[S_NEG] += neg;
+    stats[S_OB] += ob; stats[S_OT] += ovt; stats[S_EST] += est;
+    stats[S_BB] += bb; stats[S_BT] += bt;
+    return rc;
+}
+
+/* hrpp/tracer.py:343-371.  mode: 0 baseline, 1 limit, 2 live, 3 fast.
  * Outputs (found,t,slot,leaf) are the rays shading would use (base for
  * baseline/limit, live hits for live).  base_* (u,v,box,tri,vis) optional.
  * keys_out optional.  anc = go-up LUT of the table's level (NULL in baseline). */
@@ -509,6 +650,11 @@ int or_trace_wave(BVH_ARGS, const int32_t *anc, or_table *table, int p, int mode
     if (mode == 2) {
         rc = consult_live(table, &bv, closest, keys, O, D, tmins, tmaxs, n, stats, found, t, slot,
                           leaf, NULL, 0);
+        goto done;
+    }
+    if (mode == 3) {
+        rc = fast_wave(table, &bv, closest, keys, O, D, tmins, tmaxs, n, stats, found, t, slot,
+                       leaf);
         goto done;
     }
     {
@@ -548,7 +694,7 @@ int or_trace_wave_sharded(BVH_ARGS, const int32_t *anc, or_table **tables, int s
                           double *t, int32_t *slot, int32_t *leaf, double *u, double *v,
                           int64_t *box, int64_t *tri, int64_t *vis, uint64_t *keys_out,
                           int64_t *stats) {
-    if (mode == 0 || shards < 1 || shards > 65535) return OR_INVALID;
+    if (mode < 1 || mode > 2 || shards < 1 || shards > 65535) return OR_INVALID;
     BVH_INIT(bv);
     bv.anc = anc;
     stats[S_RAYS] += n;

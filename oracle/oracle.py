@@ -117,6 +117,8 @@ def _declare(L):
     L.or_trace_wave_sharded.restype = C.c_int
     L.or_build_bvh.argtypes = [P, P, P, P, I64, C.c_int, C.c_int] + [P] * 13 + [P, P, P]
     L.or_build_bvh.restype = C.c_int
+    L.or_set_fast_rounds.argtypes = [C.c_int]
+    L.or_set_fast_rounds.restype = None
 
 
 def _p(a):
@@ -371,7 +373,7 @@ class ShardedTable:
                 + "]" for i, k in enumerate(keys)]
 
 
-MODES = {"baseline": 0, "limit": 1, "live": 2}
+MODES = {"baseline": 0, "limit": 1, "live": 2, "fast": 3}
 
 
 def trace_wave(bvh: OracleBvh, table, mode, closest, O, D, tmins, tmaxs, stats=None,
@@ -384,7 +386,7 @@ def trace_wave(bvh: OracleBvh, table, mode, closest, O, D, tmins, tmaxs, stats=N
     stats = np.zeros(11, np.int64) if stats is None else stats
     out = {"found": np.zeros(n, np.bool_), "t": np.zeros(n), "slot": np.zeros(n, np.int32),
            "leaf": np.zeros(n, np.int32)}
-    if m != 2:
+    if m in (0, 1):
         if closest:
             out["u"] = np.zeros(n)
             out["v"] = np.zeros(n)
@@ -437,6 +439,11 @@ def predict_batch(bvh: OracleBvh, table: OracleTable, closest, keys, O, D, tmins
     if rc != OK:
         raise OracleError(rc, "predict_batch")
     return out
+
+
+def set_fast_rounds(rounds: int):
+    """Speculation rounds of the fast mode (oracle/hrpp_oracle.c fast_wave)."""
+    lib().or_set_fast_rounds(int(rounds))
 
 
 def max_threads():

@@ -199,3 +199,35 @@ def test_sharded_oracle_equals_reference(oracle_mod, p, g_, mode, shards):
         for k in ("found", "t", "slot", "leaf"):
             assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
         assert tables[closest].dump_lines() == list(ref[f"{w}_dump"])
+
+
+@pytest.mark.parametrize("p,g_", SETTINGS)
+def test_fast_mode_many_rounds_matches_reference_live(oracle_mod, p, g_):
+    """Fast mode's speculation rounds replay the live loop: with enough
+    rounds every ray sees exactly the appends of the rays before it, so the
+    classification, traversal counters, occlusion hits and table equal the
+    reference's live mode (hrpp/tracer.py:295-331); closest-hit TPs may
+    skip nodes appended between their own round and their turn, which only
+    moves the overhead/est counters (and t on a closer later node)."""
+    inp = load_golden("wave_inputs.npz")
+    ref = load_golden(f"wave_live_p{p}_g{g_}.npz")
+    b = obvh(oracle_mod, "spheres")
+    oracle_mod.set_fast_rounds(100000)
+    try:
+        tables = {c: oracle_mod.OracleTable(p, g_, c) for c in (True, False)}
+        for w in WAVES:
+            closest = w != "shadow"
+            rc, out, st = oracle_mod.trace_wave(b, tables[closest], "fast", closest,
+                                                inp[f"{w}_O"], inp[f"{w}_D"], inp[f"{w}_tmin"],
+                                                inp[f"{w}_tmax"])
+            assert rc == 0
+            want = ref[f"{w}_stats"]
+            same = [0, 1, 2, 3, 4, 5] if closest else list(range(11))
+            assert np.array_equal(st[same], want[same]), (w, st, want)
+            assert np.array_equal(out["found"], ref[f"{w}_found"])
+            if not closest:
+                for k in ("t", "slot", "leaf"):
+                    assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
+            assert tables[closest].dump_lines() == list(ref[f"{w}_dump"]), w
+    finally:
+        oracle_mod.set_fast_rounds(4)
