@@ -47,6 +47,11 @@ extern "C" {
 #define HRPP_MODE_BASELINE 0
 #define HRPP_MODE_LIMIT 1
 #define HRPP_MODE_LIVE 2
+/* Sort-free live mode: the live loop of
+ * hrpp/tracer.py:295-331 as key-parallel speculation rounds; exact up to the
+ * round limit (hrpp_set_fast_rounds), statistics within the tolerance
+ * DESIGN.md states beyond it.  Deterministic. */
+#define HRPP_MODE_FAST 3
 
 typedef struct hrpp_bvh_s *hrpp_bvh_t;
 typedef struct hrpp_table_s *hrpp_table_t;
@@ -245,6 +250,13 @@ int hrpp_profile_read(double *ms, int64_t *counts, int n, int reset);
 /* Live-mode speculation policy (rounds of exact per-key scan before the
  * speculative round).  Default 0.  Affects speed only, never results. */
 int hrpp_set_live_rounds(int rounds);
+/* Fast mode's speculation policy: at most `rounds` rounds (default 8), and
+ * no further round once one resolved fewer than n / stop_div of the wave's
+ * n rays (default 32; 0 = never stop early).  Every ray decided within the
+ * rounds sees exactly the appends of the rays before it; the rest are
+ * traced.  Affects statistics within the stated tolerance, never found
+ * flags or table_entries. */
+int hrpp_set_fast_rounds(int rounds, int stop_div);
 /* Key segments with at most `len` rays are replayed by one lane, longer ones
  * by a whole warp (default 32).  Affects speed only, never results. */
 int hrpp_set_consult_short(int len);

@@ -497,7 +497,9 @@ static int consult_live(or_table *t, const or_bvh *b, int closest, const uint64_
  *           its turn) or FP, traced from the root (final).  If it hit and
  *           its node anc[leaf] is new to the entry, every later unresolved
  *           ray of the key evaluates that node: a hit makes it a TP;
- *  final    the rays still unresolved after R rounds are traced (NEG or FP).
+ *  final    the rays still unresolved after R rounds are traced (NEG or FP);
+ *           the rounds also end early, before round k >= 2, when round k-1
+ *           resolved fewer than n / stop_div rays (deterministic counts).
  * Records (key, anc[leaf]) of every traced ray with a hit are applied after
  * the wave in ray order with set semantics (hrpp/predictor.py:147-160).
  * Every ray's decision sees exactly the nodes earlier rays appended, as in
@@ -508,8 +510,11 @@ static int consult_live(or_table *t, const or_bvh *b, int closest, const uint64_
  * TPs; DESIGN.md states the measured tolerance).  Counters: overhead = every
  * entry/node evaluation, baseline = the traced rays' traversals, est over
  * TPs with the ray's total evaluation boxes. */
-static int g_fast_rounds = 4;
-void or_set_fast_rounds(int r) { g_fast_rounds = r < 0 ? 0 : r; }
+static int g_fast_rounds = 8, g_fast_stop_div = 32;
+void or_set_fast_rounds(int r, int stop_div) {
+    g_fast_rounds = r < 0 ? 0 : r;
+    g_fast_stop_div = stop_div < 0 ? 0 : stop_div;
+}
 
 typedef struct { int64_t cap; int64_t *ray; } key_map;   /* key -> ray (first/last seen) */
 
@@ -561,8 +566,12 @@ static int fast_wave(or_table *t, const or_bvh *b, int closest, const uint64_t *
         }
         unres[nu++] = i;
     }
+    int64_t resolved = 0;
+    int stopped = 0;
     for (int round = 0; round <= g_fast_rounds && nu > 0; round++) {
-        const int last = round == g_fast_rounds;
+        if (round >= 1 && g_fast_stop_div > 0 && resolved * g_fast_stop_div < n) stopped = 1;
+        resolved = 0;
+        const int last = round == g_fast_rounds || stopped;
         for (int64_t h = 0; h < lead.cap; h++) lead.ray[h] = -1;
         int64_t keep = 0;
         for (int64_t u = 0; u < nu; u++) {
@@ -606,6 +615,7 @@ static int fast_wave(or_table *t, const or_bvh *b, int closest, const uint64_t *
                 evbox[i] += r.boxes;
                 if (r.found) {
                     tp++;
+                    resolved++;
                     int64_t x = (int64_t)b->depth[r.leaf] + 1 - evbox[i];
                     est += x > 0 ? x : 0;
                     ofound[i] = 1; ot_[i] = r.t; oslot[i] = (int32_t)r.slot; oleaf[i] = (int32_t)r.leaf;
@@ -615,6 +625,7 @@ static int fast_wave(or_table *t, const or_bvh *b, int closest, const uint64_t *
             unres[keep++] = i;
         }
         nu = keep;
+        if (last) break;
     }
     int rc = OR_OK;
     for (int64_t i = 0; i < n && rc == OR_OK; i++)

@@ -117,7 +117,7 @@ def _declare(L):
     L.or_trace_wave_sharded.restype = C.c_int
     L.or_build_bvh.argtypes = [P, P, P, P, I64, C.c_int, C.c_int] + [P] * 13 + [P, P, P]
     L.or_build_bvh.restype = C.c_int
-    L.or_set_fast_rounds.argtypes = [C.c_int]
+    L.or_set_fast_rounds.argtypes = [C.c_int, C.c_int]
     L.or_set_fast_rounds.restype = None
 
 
@@ -441,9 +441,9 @@ def predict_batch(bvh: OracleBvh, table: OracleTable, closest, keys, O, D, tmins
     return out
 
 
-def set_fast_rounds(rounds: int):
-    """Speculation rounds of the fast mode (oracle/hrpp_oracle.c fast_wave)."""
-    lib().or_set_fast_rounds(int(rounds))
+def set_fast_rounds(rounds: int = 8, stop_div: int = 32):
+    """Fast mode's speculation policy (oracle/hrpp_oracle.c fast_wave)."""
+    lib().or_set_fast_rounds(int(rounds), int(stop_div))
 
 
 def max_threads():

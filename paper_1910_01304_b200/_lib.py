@@ -21,7 +21,7 @@ LIB_PATH = Path(os.environ.get("HRPP_LIB") or
 
 OK, NONFINITE, CAPACITY, INVALID_ARG, CUDA_ERR = 0, 1, 2, 3, 4
 HIT_ANY, CLOSEST_HIT = 0, 1
-MODE_BASELINE, MODE_LIMIT, MODE_LIVE = 0, 1, 2
+MODE_BASELINE, MODE_LIMIT, MODE_LIVE, MODE_FAST = 0, 1, 2, 3
 STATS_LEN = 11
 
 P = C.c_void_p
@@ -49,6 +49,7 @@ def _load():
     L.hrpp_launch_count.restype = I64
     L.hrpp_device_count.argtypes = [P]
     L.hrpp_set_live_rounds.argtypes = [C.c_int]
+    L.hrpp_set_fast_rounds.argtypes = [C.c_int, C.c_int]
     L.hrpp_set_consult_short.argtypes = [C.c_int]
     L.hrpp_gen_primary.argtypes = [P, P, C.c_double, C.c_double, I64, I64, I64, I64, I64,
                                    C.c_uint64, C.c_int, P, P, P]
@@ -83,7 +84,8 @@ def _load():
     L.hrpp_predict_batch.argtypes = [P, P, P, P, P, P, P, I64] + [P] * 10 + [P]
     L.hrpp_trace_wave.argtypes = [P, P, C.c_int, C.c_int, P, P, P, P, I64, C.POINTER(WaveOut),
                                   C.POINTER(OutcomeLogC), P, P]
-    for name in ("hrpp_device_count", "hrpp_set_live_rounds", "hrpp_hash_rays",
+    for name in ("hrpp_device_count", "hrpp_set_live_rounds", "hrpp_set_fast_rounds",
+                 "hrpp_hash_rays",
                  "hrpp_hash_floats", "hrpp_coarsen_keys", "hrpp_bvh_create", "hrpp_bvh_destroy",
                  "hrpp_bvh_ancestor_lut", "hrpp_build_bvh", "hrpp_trace_batch",
                  "hrpp_table_create", "hrpp_table_destroy", "hrpp_table_clear",
@@ -119,7 +121,8 @@ EXPORTED = ("hrpp_last_error", "hrpp_version", "hrpp_launch_count", "hrpp_device
             "hrpp_table_destroy", "hrpp_table_clear", "hrpp_table_clear_async", "hrpp_table_info",
             "hrpp_table_record",
             "hrpp_table_lookup", "hrpp_table_export", "hrpp_predict_batch", "hrpp_trace_wave",
-            "hrpp_set_live_rounds", "hrpp_profile_enable", "hrpp_profile_read",
+            "hrpp_set_live_rounds", "hrpp_set_fast_rounds", "hrpp_profile_enable",
+            "hrpp_profile_read",
             "hrpp_table_set_deferred", "hrpp_table_pending", "hrpp_set_consult_short",
             "hrpp_gen_primary", "hrpp_spawn", "hrpp_partition_by_owner",
             "hrpp_profile_stages", "hrpp_pack_rays", "hrpp_unpack_rays", "hrpp_pack_hits",

@@ -29,8 +29,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-warn-spills",
               f"-I{ROOT / 'include'}", f"-I{CSRC}"]
-SOURCES = ["k_hash_trace.cu", "k_table.cu", "k_consult.cu", "k_spawn.cu", "k_shard.cu", "capi.cu",
-           "bvh_build.cpp"]
+SOURCES = ["k_hash_trace.cu", "k_table.cu", "k_consult.cu", "k_fast.cu", "k_spawn.cu", "k_shard.cu",
+           "capi.cu", "bvh_build.cpp"]
 
 
 def nvcc() -> str:

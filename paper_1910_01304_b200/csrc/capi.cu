@@ -329,6 +329,13 @@ int hrpp_profile_read(double* ms, int64_t* counts, int n, int reset) {
     }
   return P_NCAT;
 }
+int hrpp_set_fast_rounds(int rounds, int stop_div) {
+  CHECK_ARG(rounds >= 0 && rounds < 100000, "fast rounds must be in [0, 100000)");
+  CHECK_ARG(stop_div >= 0, "stop_div must be >= 0");
+  g_fast_rounds = rounds;
+  g_fast_stop_div = stop_div;
+  return HRPP_OK;
+}
 int hrpp_set_live_rounds(int rounds) {
   CHECK_ARG(rounds >= 0 && rounds < 1000, "live rounds must be in [0, 1000)");
   g_live_rounds = rounds;
@@ -732,7 +739,10 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
                     const float* D, const double* tmin, const double* tmax, int64_t n,
                     hrpp_wave_out* out, hrpp_outcome_log* log, int64_t* stats, void* stream) {
   CHECK_ARG(bvh && stats, "null argument");
-  CHECK_ARG(mode >= HRPP_MODE_BASELINE && mode <= HRPP_MODE_LIVE, "bad mode");
+  CHECK_ARG(mode >= HRPP_MODE_BASELINE && mode <= HRPP_MODE_FAST, "bad mode");
+  CHECK_ARG(mode != HRPP_MODE_FAST || !t || !t->deferred,
+            "fast mode does not support deferred commits");
+  const bool live_like = mode == HRPP_MODE_LIVE || mode == HRPP_MODE_FAST;
   CHECK_ARG(mode == HRPP_MODE_BASELINE || t, "limit and live modes need a table");
   CHECK_ARG(!t || mode == HRPP_MODE_BASELINE || t->closest == (closest != 0),
             "table kind does not match the wave's ray kind");
@@ -758,7 +768,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
       (rc = sg.out(out->slot, n, &to.slot)) || (rc = sg.out(out->leaf, n, &to.leaf)) ||
       (rc = sg.out(out->keys, n, &keys)))
     return rc;
-  if (mode != HRPP_MODE_LIVE) {
+  if (!live_like) {
     if ((rc = sg.out(out->box, n, &to.box)) || (rc = sg.out(out->tri, n, &to.tri)) ||
         (rc = sg.out(out->visited, n, &to.vis)))
       return rc;
@@ -778,7 +788,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
         (rc = sg.need(&to.leaf, n)))
       return rc;
     if (mode == HRPP_MODE_LIMIT && (rc = sg.need(&to.box, n))) return rc;
-    if (mode == HRPP_MODE_LIVE && (rc = sg.need(&to.slot, n))) return rc;
+    if (live_like && (rc = sg.need(&to.slot, n))) return rc;
   }
   int* err;
   unsigned long long* sdev;
@@ -788,20 +798,24 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
   HRPP_CK(cudaMemsetAsync(sdev, 0, sizeof(unsigned long long) * 17, st));
   // keys nobody asked for go straight into the grouping sort's packed form
   bool prepacked = false;
-  if (mode != HRPP_MODE_BASELINE) {
+  if (mode == HRPP_MODE_FAST) {  // hashing is fused into the fast consult
+    FastIO io{dO, dD, d0, d1, n, to.found, to.t, to.slot, to.leaf, keys};
+    if ((rc = run_fast(*bvh, *t, io, sdev, err, st))) return rc;
+    if ((rc = read_meta_and_finish(*t, err, st, sg, sdev))) return rc;
+  } else if (mode != HRPP_MODE_BASELINE) {
     int ib = 1;  // ray index bits, as group_by_key computes them
     while (ib < 31 && (1ll << ib) < n) ib++;
     prepacked = out->keys == nullptr && 3 * (1 + 2 * t->precision) + ib <= 64;
     if ((rc = launch_hash(dO, dD, n, t->precision, keys, err, st, prepacked ? ib : 0)))
       return rc;
   }
-  if (mode != HRPP_MODE_LIVE) {
+  if (!live_like) {
     to.sums = sdev + 4;  // baseline_box_tests, baseline_tri_tests (tracer.py:361-362)
     if ((rc = launch_trace(*bvh, closest != 0, dO, dD, d0, d1, 0, n, nullptr, nullptr, to, err,
                            st, &ws)))
       return rc;
   }
-  if (mode != HRPP_MODE_BASELINE) {
+  if (mode != HRPP_MODE_BASELINE && mode != HRPP_MODE_FAST) {
     Consult c;
     c.live = mode == HRPP_MODE_LIVE;
     c.O = dO;
@@ -823,7 +837,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
     c.log_pred_slot = lg.pred_slot;
     if ((rc = run_consult(*bvh, *t, c, keys, sdev, err, st, prepacked))) return rc;
     if ((rc = read_meta_and_finish(*t, err, st, sg, sdev))) return rc;
-  } else {
+  } else if (mode == HRPP_MODE_BASELINE) {
     if ((rc = g_pinned.get())) return rc;
     if ((rc = to_host(g_pinned.p + 3, err, sizeof(int), st))) return rc;
     if ((rc = to_host(g_pinned.p + 4, sdev, sizeof(long long) * 16, st))) return rc;
@@ -850,7 +864,7 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
     return HRPP_CUDA;
   }
   for (int k = 1; k < HRPP_STATS_LEN; k++)
-    if (!((mode != HRPP_MODE_LIVE) && (k == 4 || k == 5))) stats[k] += s[k];
+    if (live_like || !(k == 4 || k == 5)) stats[k] += s[k];
   return HRPP_OK;
 }
 

@@ -129,6 +129,25 @@ __device__ __forceinline__ int32_t slot_leaf(const DTri* __restrict__ tris, int3
 #endif
 }
 
+// Ray hash of one float (hrpp/rayhash.py:67-78, :118-122): sign, top p
+// exponent bits, top p mantissa bits.
+__device__ __forceinline__ uint32_t lane_hash(uint32_t bits, int p) {
+  uint32_t sign = bits >> 31;
+  uint32_t exp_top = ((bits >> 23) & 0xFFu) >> (8 - p);
+  uint32_t man_top = (bits & 0x7FFFFFu) >> (23 - p);
+  return (sign << (2 * p)) | (exp_top << p) | man_top;
+}
+
+__device__ __forceinline__ bool nonfinite(uint32_t b) { return ((b >> 23) & 0xFFu) == 0xFFu; }
+
+// LANE_PAIRS ((0,2),(1,1),(2,0)) at shifts 0/16/32 (hrpp/rayhash.py:37-39)
+__device__ __forceinline__ uint64_t ray_key(uint32_t ox, uint32_t oy, uint32_t oz, uint32_t dx,
+                                            uint32_t dy, uint32_t dz, int p) {
+  return (uint64_t)(lane_hash(ox, p) ^ lane_hash(dz, p)) |
+         ((uint64_t)(lane_hash(oy, p) ^ lane_hash(dy, p)) << 16) |
+         ((uint64_t)(lane_hash(oz, p) ^ lane_hash(dx, p)) << 32);
+}
+
 constexpr double kDetEps = 1e-9;          // hrpp/kernels.py:20
 constexpr double kWrongClosestEps = 1e-9; // hrpp/tracer.py:52
 

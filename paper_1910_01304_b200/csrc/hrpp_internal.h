@@ -125,6 +125,7 @@ struct TableDev {
   bool deferred = false;
   int64_t pending = 0;
   double start_tp_frac = 1.0;  // wave-start TP fraction of the last live wave
+  int64_t fast_wcap = 0;  // fast mode: initialised wave-slot capacity
   // stream-ordered clear: every later call on the table waits for it
   cudaEvent_t clear_ev = nullptr;
   bool clear_recorded = false;
@@ -227,6 +228,23 @@ int set_i32(int32_t* dst, int32_t v, cudaStream_t st);
 int set_i64(long long* dst, long long v, cudaStream_t st);
 
 extern int g_live_rounds;
+
+// Fast mode (k_fast.cu): the wave's rays and outputs (device pointers).
+struct FastIO {
+  const float* O;
+  const float* D;
+  const double* tmin;
+  const double* tmax;
+  int64_t n;
+  uint8_t* found;
+  double* t;
+  int32_t* slot;
+  int32_t* leaf;
+  uint64_t* keys;
+};
+extern int g_fast_rounds, g_fast_stop_div;
+int run_fast(const BvhDev& b, TableDev& t, const FastIO& io, unsigned long long* stats_dev,
+             int* err, cudaStream_t st);
 
 inline int grid_for(int64_t n, int block, int max_blocks) {
   int64_t g = (n + block - 1) / block;

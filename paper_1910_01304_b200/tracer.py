@@ -38,10 +38,13 @@ class RenderMode(Enum):
     BASELINE = "baseline"
     LIMIT = "limit"
     LIVE = "live"
+    # extension (no reference counterpart): live mode without the grouping
+    # sort, as R key-parallel speculation rounds
+    FAST = "fast"
 
 
 _MODE = {RenderMode.BASELINE: _lib.MODE_BASELINE, RenderMode.LIMIT: _lib.MODE_LIMIT,
-         RenderMode.LIVE: _lib.MODE_LIVE}
+         RenderMode.LIVE: _lib.MODE_LIVE, RenderMode.FAST: _lib.MODE_FAST}
 
 # RayKindStats field order (hrpp/metrics.py:38-51) = the C ABI's stats order
 STATS_FIELDS = ("rays", "tp", "fp", "neg", "baseline_box_tests", "baseline_tri_tests",
@@ -80,6 +83,16 @@ class OutcomeLog:
 def set_live_rounds(rounds: int):
     """Exact consult rounds before the speculative round (speed only)."""
     _lib.check(_lib.lib.hrpp_set_live_rounds(int(rounds)), "set_live_rounds")
+
+
+FAST_ROUNDS, FAST_STOP_DIV = 8, 32  # the library's defaults
+
+
+def set_fast_rounds(rounds: int = FAST_ROUNDS, stop_div: int = FAST_STOP_DIV):
+    """Fast mode's speculation policy: at most ``rounds`` rounds, none after
+    a round that resolved fewer than n / stop_div rays (0: never stop early).
+    Moves statistics within the stated tolerance, never found flags."""
+    _lib.check(_lib.lib.hrpp_set_fast_rounds(int(rounds), int(stop_div)), "set_fast_rounds")
 
 
 def set_consult_short(length: int):
@@ -122,7 +135,7 @@ def trace_wave(bvh: Bvh, table: Optional[PredictorTable], mode: RenderMode, O, D
     for k, dt in (("found", np.bool_), ("t", np.float64), ("slot", np.int32),
                   ("leaf", np.int32)):
         want(k, dt)
-    if mode is not RenderMode.LIVE:
+    if mode not in (RenderMode.LIVE, RenderMode.FAST):
         if closest:
             want("u", np.float64)
             want("v", np.float64)

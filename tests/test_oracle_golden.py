@@ -212,7 +212,7 @@ def test_fast_mode_many_rounds_matches_reference_live(oracle_mod, p, g_):
     inp = load_golden("wave_inputs.npz")
     ref = load_golden(f"wave_live_p{p}_g{g_}.npz")
     b = obvh(oracle_mod, "spheres")
-    oracle_mod.set_fast_rounds(100000)
+    oracle_mod.set_fast_rounds(100000, 0)
     try:
         tables = {c: oracle_mod.OracleTable(p, g_, c) for c in (True, False)}
         for w in WAVES:
@@ -230,4 +230,4 @@ def test_fast_mode_many_rounds_matches_reference_live(oracle_mod, p, g_):
                     assert np.array_equal(out[k], ref[f"{w}_{k}"]), (w, k)
             assert tables[closest].dump_lines() == list(ref[f"{w}_dump"]), w
     finally:
-        oracle_mod.set_fast_rounds(4)
+        oracle_mod.set_fast_rounds()
