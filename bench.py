@@ -341,6 +341,26 @@ def run_ours(args, rank, world, local_rank):
         frame("baseline")
     ms_base = timed(lambda: frame("baseline"), args.steps)
     base_value = n_total * args.steps / (ms_base * 1e-3) / 1e6
+
+    # ---- fast mode (sort-free speculation rounds) -------------
+    fast = None
+    if not multi:
+        for _ in range(2):
+            frame("fast")
+        ms_fast = timed(lambda: frame("fast"), args.steps)
+        fast_stats = {k: np.zeros(11, np.int64) for k in kinds}
+        frame("fast", stats=fast_stats)
+        fast = {"mrays_s": round(n_total * args.steps / (ms_fast * 1e-3) / 1e6, 3),
+                "ms_per_step": round(ms_fast / args.steps, 4),
+                "speedup_vs_full_traversal": round(ms_base / ms_fast, 4),
+                "policy": {"max_rounds": hb.tracer.FAST_ROUNDS,
+                           "stop_div": hb.tracer.FAST_STOP_DIV},
+                "stats": {k: dict(zip(STATS_NAMES, map(int, fast_stats[k]))) for k in kinds},
+                "tp_rel_vs_exact_live": {
+                    k: round((int(fast_stats[k][1]) - int(live_stats[k][1]))
+                             / max(1, int(live_stats[k][1])), 4) for k in kinds},
+                "note": "statistics within the stated tolerance of exact live mode "
+                        "(tests/test_fast_mode.py); found flags and table_entries exact"}
     lim_stats = {k: np.zeros(11, np.int64) for k in kinds}
     frame("limit", stats=lim_stats)
     tstats = {}
@@ -402,12 +422,23 @@ def run_ours(args, rank, world, local_rank):
     d_bytes = alg[dom] / max(1, tq[1] / steps)
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
-        traffic = json.loads(tp.read_text()).get(dom)
+    if tp.exists():  # ncu DRAM bytes per launch of the stage, by config
+        traffic = json.loads(tp.read_text()).get(args.config, {}).get(dom)
     achieved = d_bytes / (d_ms * 1e-3) / 1e9
     roofline = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                "achieved_note": "algorithmic bytes (SURVEY 8(d): 32 B/box test, 36 B/tri test, "
+                                 "64 B/ray I/O) per launch / mean launch time"}
+    if traffic:
+        dram = traffic / (d_ms * 1e-3) / 1e9
+        roofline.update(dram_achieved=round(dram, 2), dram_frac=round(dram / peak, 4))
+    if dom.startswith("trace"):
+        roofline["bound_note"] = (
+            "the traversal's node/triangle reads mostly hit L1/L2 (c5: 56 % L2, 61 % L1 "
+            "hit rate; profiles/r2_c5_trace_full.md): it is bound by dependent-load latency "
+            "and SIMT divergence (~10 of 32 lanes active), not by DRAM bandwidth; dram_frac "
+            "is the HBM share actually used")
 
     # ---- e2e: host buffers through the public API ------------------------------------
     # Every step copies each wave's inputs from pinned host memory and its hits
@@ -534,7 +565,7 @@ def run_ours(args, rank, world, local_rank):
                            "traces on a side stream concurrently with its grouping, so "
                            "group and trace_queue overlap and the stages sum past the frame; "
                            "the roofline stage alone is event-timed inside the timed region",
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "fast_mode": fast,
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(line))
