@@ -43,31 +43,29 @@ def _backend_device(dist, group=None):
     return torch.device("cpu")
 
 
-def all_gather_varlen(dist, arr: np.ndarray, group=None) -> list:
-    """All-gather 1-D numpy arrays of different lengths (pad to the max)."""
+def all_gather_varlen(dist, t, group=None) -> list:
+    """All-gather 1-D tensors of different lengths (padded to the longest):
+    the list of every rank's tensor, in rank order, on the backend's
+    device (NCCL: device-resident, nothing passes through the host)."""
     import torch
     dev = _backend_device(dist, group)
     world = dist.get_world_size(group)
-    n = torch.tensor([arr.shape[0]], dtype=torch.int64, device=dev)
+    t = torch.as_tensor(t).to(dev)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
     sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
     sizes = [int(s.item()) for s in sizes]
-    m = max(sizes) if sizes else 0
-    view = arr.view(np.int64) if arr.dtype == np.uint64 else arr
-    buf = np.zeros(max(m, 1), dtype=view.dtype)
-    buf[:arr.shape[0]] = view
-    t = torch.from_numpy(buf).to(dev)
-    outs = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(outs, t, group=group)
-    res = []
-    for o, s in zip(outs, sizes):
-        a = o.cpu().numpy()[:s]
-        res.append(a.view(np.uint64) if arr.dtype == np.uint64 else a)
-    return res
+    m = max(max(sizes), 1)
+    buf = torch.zeros(m, dtype=t.dtype, device=dev)
+    buf[:t.shape[0]] = t
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    return [o[:s] for o, s in zip(outs, sizes)]
 
 
 def merge_records(parts_keys, parts_nodes, parts_rays, offsets):
-    """Concatenate per-rank records and order them by global ray index."""
+    """Host restatement of the merge (tests): concatenate per-rank records
+    and order them by global ray index."""
     if not parts_keys:
         return np.zeros(0, np.uint64), np.zeros(0, np.int32)
     keys = np.concatenate(parts_keys).astype(np.uint64)
@@ -79,15 +77,33 @@ def merge_records(parts_keys, parts_nodes, parts_rays, offsets):
 
 def merge_wave_records(table, dist, ray_offset: int = 0, group=None):
     """Exchange the last deferred wave's records and apply them in global ray
-    order on every rank (the collective step between waves)."""
-    keys, nodes, rays = table.pending_records()
-    k_all = all_gather_varlen(dist, keys, group)
-    n_all = all_gather_varlen(dist, nodes, group)
-    r_all = all_gather_varlen(dist, rays, group)
-    o_all = all_gather_varlen(dist, np.array([ray_offset], np.int64), group)
-    mk, mn = merge_records(k_all, n_all, r_all, [int(o[0]) for o in o_all])
+    order on every rank (the collective step between waves).
+
+    Every rank holds a contiguous block of the wave, blocks in rank order,
+    and its records are sorted by ray index within the block, so the ranks'
+    records concatenated in rank order ARE the wave's records in global ray
+    order: one all-gather (NCCL over NVLink: device tensors end to end) and
+    one sequential-semantics ``record_batch`` on the device.  ``ray_offset``
+    (this block's first global ray) is checked to be non-decreasing in rank
+    order."""
+    import torch
+    dev = _backend_device(dist, group)
+    keys, nodes, _ = table.pending_records(device=dev.type == "cuda")
+    if isinstance(keys, np.ndarray):
+        keys, nodes = torch.from_numpy(keys.view(np.int64)), torch.from_numpy(nodes)
+    else:
+        keys = keys.view(torch.int64)
+    offs = [int(o.item()) for o in all_gather_varlen(
+        dist, torch.tensor([ray_offset], dtype=torch.int64), group)]
+    if any(b < a for a, b in zip(offs, offs[1:])):
+        raise ValueError("ray blocks must be in rank order")
+    mk = torch.cat(all_gather_varlen(dist, keys, group))
+    mn = torch.cat(all_gather_varlen(dist, nodes, group))
     if mk.shape[0]:
-        table.record_batch(mk, mn)
+        if dev.type == "cuda":
+            table.record_batch(mk.view(torch.uint64), mn)
+        else:
+            table.record_batch(mk.numpy().view(np.uint64), mn.numpy())
     return int(mk.shape[0])
 
 

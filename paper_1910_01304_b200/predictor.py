@@ -225,16 +225,24 @@ class PredictorTable:
             _lib.check(_lib.lib.hrpp_table_set_deferred(self.handle, int(on)), "set_deferred")
             self._deferred = on
 
-    def pending_records(self):
+    def pending_records(self, device: bool = False):
         """(keys u64, nodes i32, ray indices i32) of the last deferred wave,
-        sorted by ray index within the wave."""
+        sorted by ray index within the wave: numpy arrays, or with ``device``
+        CUDA tensors on the table's device (a device-to-device copy)."""
         cnt = C.c_int64()
         _lib.check(_lib.lib.hrpp_table_pending(self.handle, None, None, None, 0, C.byref(cnt)),
                    "pending")
         m = cnt.value
-        keys = np.empty(m, np.uint64)
-        nodes = np.empty(m, np.int32)
-        rays = np.empty(m, np.int32)
+        if device:
+            import torch
+            dev = torch.device("cuda", self._device)
+            keys = torch.empty(m, dtype=torch.uint64, device=dev)
+            nodes = torch.empty(m, dtype=torch.int32, device=dev)
+            rays = torch.empty(m, dtype=torch.int32, device=dev)
+        else:
+            keys = np.empty(m, np.uint64)
+            nodes = np.empty(m, np.int32)
+            rays = np.empty(m, np.int32)
         if m:
             _lib.check(_lib.lib.hrpp_table_pending(self.handle, _lib.ptr(keys), _lib.ptr(nodes),
                                                    _lib.ptr(rays), m, C.byref(cnt)), "pending")

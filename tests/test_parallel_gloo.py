@@ -26,7 +26,7 @@ class FakeTable:
         self.t = oracle_mod.OracleTable(6, 0, True)
         self._p = (keys, nodes, rays)
 
-    def pending_records(self):
+    def pending_records(self, device=False):
         return self._p
 
     def record_batch(self, k, n):
