@@ -37,6 +37,7 @@ import sys
 from pathlib import Path
 
 os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/hrpp_numba_cache")
+sys.dont_write_bytecode = True  # never write __pycache__ into /root/reference
 REF = Path("/root/reference/pkg/src")
 sys.path.insert(0, str(REF))
 sys.path.insert(0, "/root/reference/pkg/tests")
