@@ -70,6 +70,53 @@ def parse():
 # workload
 # ---------------------------------------------------------------------------
 
+def make_workload_device(args):
+    """The same frame generated on the GPU (our arm): primary rays by
+    k_gen_primary, full-traversal hits on the device, shadow and bounce
+    waves by k_spawn, so the waves never leave HBM.  Bit-identical to
+    make_workload's numpy waves (tests/test_gpu_parity.py
+    test_device_waves_equal_host_waves).  Returns the same triple with CUDA
+    tensors in the waves."""
+    import paper_1910_01304_b200 as hb
+    from paper_1910_01304_b200 import scenes, waves as dwaves
+    res = tuple(int(x) for x in args.res.split("x")) if args.res else None
+    sc = scenes.make_scene(args.config, resolution=res, spp=args.spp)
+    bvh = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=sc.builder == "median")
+    O, D = dwaves.generate_primary_rays(sc.camera, sc.spp, seed=0)
+    n = O.shape[0]
+    t0 = torch_zeros(n, O.device)
+    waves = [("primary", "primary", True, O, D, t0, torch_inf(n, O.device))]
+    cur = waves[0]
+    for level in range(sc.bounces + 1):
+        _, _, _, Oc, Dc, a, b = cur
+        base = hb.intersect_closest_batch(bvh, Oc, Dc, a, b)
+        lights = ([("area", sc.area_light[0], sc.area_light[1])] if sc.area_light is not None
+                  else [("point", lp) for lp in sc.point_lights])
+        shadow = level < sc.bounces or level == 0
+        bounce = "diffuse" if level < sc.bounces else None
+        for li, light in enumerate(lights if shadow else [None]):
+            sp = dwaves.spawn_secondary(bvh, Oc, Dc, base, shadow=light,
+                                        bounce=bounce if li == 0 else None, seed=level)
+            if light is not None:
+                waves.append((f"shadow{level}_{li}", "shadow", False, *sp["shadow"]))
+            if li == 0 and bounce:
+                nxt = (f"bounce{level + 1}", "bounce", True, *sp["bounce"])
+        if level < sc.bounces:
+            cur = nxt
+            waves.append(cur)
+    return sc, bvh, waves
+
+
+def torch_zeros(n, dev):
+    import torch
+    return torch.zeros(n, dtype=torch.float64, device=dev)
+
+
+def torch_inf(n, dev):
+    import torch
+    return torch.full((n,), float("inf"), dtype=torch.float64, device=dev)
+
+
 def make_workload(args, trace_closest=None, build=None):
     """Scene, BVH and the ordered waves of one frame (host numpy).
 
@@ -231,17 +278,17 @@ def run_ours(args, rank, world, local_rank):
     if args.consult_short is not None:
         hb.set_consult_short(args.consult_short)
 
-    def gpu_trace(bvh, O, D, t0, t1):
-        return hb.intersect_closest_batch(bvh, O, D, t0, t1)
-
-    sc, bvh, waves = make_workload(args, gpu_trace)
+    # the frame's waves generated on the device (never leave HBM); host copies
+    # (outside any timed region) feed the e2e leg and the CPU baseline
+    sc, bvh, gen_waves = make_workload_device(args)
+    waves = [(*w[:3], *(a.cpu().numpy() for a in w[3:])) for w in gen_waves]
     cfg = hb.HashConfig(args.precision)
     tables = {True: hb.PredictorTable(cfg, args.go_up, hb.RayKind.CLOSEST_HIT, device=local_rank),
               False: hb.PredictorTable(cfg, args.go_up, hb.RayKind.HIT_ANY, device=local_rank)}
     my = [shard(w, rank, world) for w in waves]
     offsets = [(w[3].shape[0] * rank) // world for w in waves]
-    to_dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-    dwaves = [(w[2], *(to_dev(a) for a in w[3:])) for w in my]
+    dwaves = [(w[2], *(a.contiguous() for a in w[3:]))
+              for w in (shard(g, rank, world) for g in gen_waves)]
     n_local = sum(w[1].shape[0] for w in dwaves)
     n_total = sum(w[3].shape[0] for w in waves)
     kinds = sorted({w[1] for w in waves}, key=KINDS.index)

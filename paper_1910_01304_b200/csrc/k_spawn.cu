@@ -14,7 +14,8 @@
 //                 Point-light shadows and mirror bounces are bit-identical
 //                 to the reference renderer's numpy arithmetic; area-light
 //                 and diffuse spawns (absent from the reference) are
-//                 deterministic in (seed, hit index).
+//                 bit-identical to this repo's host generators
+//                 (scenes.area_light_samples, scenes.cosine_bounce).
 #include <cub/cub.cuh>
 
 #include "../../include/hrpp_b200.h"
@@ -100,6 +101,34 @@ struct SpawnArgs {
   double *b0, *b1;
 };
 
+// (cos, sin) of 2 pi u, u in [0, 1): scenes.cos_sin_turn's plain float64
+// operations in the same order (no FMA: the library is built with
+// --fmad=false), so diffuse bounces match the host generator bit for bit.
+__device__ __forceinline__ void cos_sin_turn(double u, double* cs, double* sn) {
+  const double x = 4.0 * u;
+  const double q = floor(x);
+  const double t = (x - q) * 1.5707963267948966;
+  const double t2 = t * t;
+  const double S[8] = {-1.0 / 6, 1.0 / 120, -1.0 / 5040, 1.0 / 362880, -1.0 / 39916800,
+                       1.0 / 6227020800, -1.0 / 1307674368000, 1.0 / 355687428096000};
+  const double C[8] = {-1.0 / 2, 1.0 / 24, -1.0 / 720, 1.0 / 40320, -1.0 / 3628800,
+                       1.0 / 479001600, -1.0 / 87178291200, 1.0 / 20922789888000};
+  double s = S[7], c = C[7];
+#pragma unroll
+  for (int k = 6; k >= 0; k--) {
+    s = S[k] + t2 * s;
+    c = C[k] + t2 * c;
+  }
+  s = t * (1.0 + t2 * s);
+  c = 1.0 + t2 * c;
+  switch ((int)q & 3) {
+    case 0: *cs = c; *sn = s; break;
+    case 1: *cs = -s; *sn = c; break;
+    case 2: *cs = -c; *sn = -s; break;
+    default: *cs = s; *sn = -c; break;
+  }
+}
+
 __global__ void k_spawn(SpawnArgs a) {
   const int m = *a.count;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
@@ -164,9 +193,9 @@ __global__ void k_spawn(SpawnArgs a) {
     } else if (a.bounce_kind == 2) {  // cosine-weighted about N
       const double u1 = unit_float(a.seed, (uint64_t)j, 0, 20);
       const double u2 = unit_float(a.seed, (uint64_t)j, 0, 21);
-      const double rr = sqrt(u1), phi = 6.283185307179586 * u2;
+      const double rr = sqrt(u1);
       double sphi, cphi;
-      sincos(phi, &sphi, &cphi);
+      cos_sin_turn(u2, &cphi, &sphi);
       const double lx = rr * cphi, ly = rr * sphi, lz = sqrt(fmax(0.0, 1.0 - u1));
       double ax[3] = {1.0, 0.0, 0.0};
       if (fabs(N[0]) > 0.9) {

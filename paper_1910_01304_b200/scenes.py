@@ -355,14 +355,44 @@ def area_light_samples(n, center, half, seed, dim0=10):
     return np.stack([c[0] + (2 * u - 1) * half, np.full(n, c[1]), c[2] + (2 * v - 1) * half], 1)
 
 
+# Taylor coefficients of sin and cos on [0, pi/2] (truncation error < 5e-14)
+_SIN_C = (-1.0 / 6, 1.0 / 120, -1.0 / 5040, 1.0 / 362880, -1.0 / 39916800, 1.0 / 6227020800,
+          -1.0 / 1307674368000, 1.0 / 355687428096000)
+_COS_C = (-1.0 / 2, 1.0 / 24, -1.0 / 720, 1.0 / 40320, -1.0 / 3628800, 1.0 / 479001600,
+          -1.0 / 87178291200, 1.0 / 20922789888000)
+_HALF_PI = 1.5707963267948966
+
+
+def cos_sin_turn(u):
+    """(cos, sin) of 2 pi u for u in [0, 1): quarter-turn reduction and
+    Horner polynomials in plain float64 operations, so the device spawn
+    (csrc/k_spawn.cu, built without FMA) reproduces it bit for bit."""
+    x = 4.0 * np.asarray(u, np.float64)
+    q = np.floor(x)
+    t = (x - q) * _HALF_PI
+    t2 = t * t
+    s = _SIN_C[-1]
+    for k in _SIN_C[-2::-1]:
+        s = k + t2 * s
+    s = t * (1.0 + t2 * s)
+    c = _COS_C[-1]
+    for k in _COS_C[-2::-1]:
+        c = k + t2 * c
+    c = 1.0 + t2 * c
+    qi = q.astype(np.int64) & 3
+    cos = np.select([qi == 0, qi == 1, qi == 2], [c, -s, -c], s)
+    sin = np.select([qi == 0, qi == 1, qi == 2], [s, c, -s], -c)
+    return cos, sin
+
+
 def cosine_bounce(offset_P, N, seed, dim0=20):
     n = offset_P.shape[0]
     idx = np.arange(n, dtype=np.uint64)
     u1 = unit_floats(seed, idx, np.zeros(n, np.uint64), dim0)
     u2 = unit_floats(seed, idx, np.zeros(n, np.uint64), dim0 + 1)
     r = np.sqrt(u1)
-    phi = 2.0 * math.pi * u2
-    lx, ly, lz = r * np.cos(phi), r * np.sin(phi), np.sqrt(np.maximum(0.0, 1.0 - u1))
+    cphi, sphi = cos_sin_turn(u2)
+    lx, ly, lz = r * cphi, r * sphi, np.sqrt(np.maximum(0.0, 1.0 - u1))
     a = np.where(np.abs(N[:, 0:1]) > 0.9, np.array([[0.0, 1.0, 0.0]]), np.array([[1.0, 0, 0]]))
     tx = np.cross(N, a)
     tx /= np.linalg.norm(tx, axis=1, keepdims=True)
