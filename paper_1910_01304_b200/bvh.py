@@ -3,7 +3,8 @@
 ``Bvh`` takes the reference's flat arrays (hrpp/bvh.py:75-92: bmin/bmax
 (N,3) f32, left/right i32, axis i8, first/count i32, parent/depth i32,
 tv0/tv1/tv2 (M,3) f32, tri_ids i32) and mirrors them once into the HBM
-layout of csrc/hrpp_device.cuh (32-B nodes, 48-B triangles).  Traversal
+layout of csrc/hrpp_device.cuh (32-B float32 nodes, 96-B triangle records:
+float64 v0 and edges plus the leaf).  Traversal
 (``intersect_*``) runs the sm_100a float64 kernel; results are bit-identical
 to hrpp/kernels.py.  ``build_bvh_from_arrays`` calls the native builder
 (csrc/bvh_build.cpp), which reproduces the reference SAH builder's arrays.

@@ -676,7 +676,10 @@ __global__ void __launch_bounds__(HRPP_REPLAY_BS, HRPP_REPLAY_MINB * 128 / HRPP_
 // seg_warp's loop with a block-wide "first non-TP ray" (shared-memory
 // atomicMin between barriers).  Same order, same appends, same results.
 constexpr int kBlockReplay = 256;
-constexpr int kBlockReplayMin = 1024;
+#ifndef HRPP_BLOCK_REPLAY_MIN
+#define HRPP_BLOCK_REPLAY_MIN 1024  // segments with more rays left get a 256-thread block
+#endif
+constexpr int kBlockReplayMin = HRPP_BLOCK_REPLAY_MIN;
 
 #ifndef HRPP_BLOCK_MINB
 #define HRPP_BLOCK_MINB 2

@@ -7,8 +7,14 @@ Reference: ``_trace_wave`` (hrpp/tracer.py:343-371) with ``_consult_limit``
 * baseline -- full traversal of every ray; counters fill the denominators;
 * limit -- full traversal + the exact per-key consult/train replay; the
   returned hits are the full-traversal hits, statistics are exact;
-* live -- predict first; only rays that are not true positives are traced
-  from the root (compacted queue), then train.
+* live -- the reference's predict-or-traverse loop, exact: every ray that
+  is not a true positive at its turn gets its full traversal (from the
+  root) and trains the table in ray order.  On a table that is empty at
+  the wave start every ray is traced up front (overlapping the grouping
+  sort), since no TP is known before the wave's first appends; TPs then
+  take their entry's result.  See DESIGN.md section 6;
+* fast -- live mode as sort-free key-parallel speculation rounds, within a
+  stated tolerance of exact.
 
 ``_trace_wave`` keeps the reference's signature so the reference renderer's
 loop can call it unchanged; ``trace_wave`` is the array-level API used by

@@ -1,4 +1,4 @@
-"""GPU idle gaps inside one live c2 frame, from a CUPTI kernel timeline
+"""GPU idle gaps inside one live frame (bench --config), from a CUPTI kernel timeline
 (torch.profiler): every interval where no kernel or memcpy/memset runs, with
 the activities on either side.  Usage: python tools/gap_timeline.py [bench args]"""
 import sys
@@ -13,10 +13,8 @@ import paper_1910_01304_b200 as hb  # noqa: E402
 TL = "--timeline" in sys.argv
 sys.argv = [a for a in sys.argv if a != "--timeline"]
 args = bench.parse()
-sc, bvh, waves = bench.make_workload(args, trace_closest=lambda b, O, D, t0, t1:
-                                     hb.intersect_closest_batch(b, O, D, t0, t1))
-dev = torch.device("cuda")
-dw = [(w[2], *(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in w[3:])) for w in waves]
+sc, bvh, waves = bench.make_workload_device(args)
+dw = [(w[2], *w[3:]) for w in waves]
 cfg = hb.HashConfig(args.precision)
 tables = {c: hb.PredictorTable(cfg, args.go_up, hb.RayKind.CLOSEST_HIT if c else hb.RayKind.HIT_ANY)
           for c in (True, False)}
