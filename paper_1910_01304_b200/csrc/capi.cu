@@ -886,8 +886,10 @@ int hrpp_trace_wave(hrpp_bvh_t bvh, hrpp_table_t t, int mode, int closest, const
     stats[4] += s[4];  // the baseline sums precede the consult (tracer.py:361-362)
     stats[5] += s[5];
   }
-  if (mode == HRPP_MODE_LIVE && t && e == 0)  // slot 14: wave-start TPs (k_eval0)
+  if (mode == HRPP_MODE_LIVE && t && e == 0) {  // slot 14: wave-start TPs (k_eval0)
     t->start_tp_frac = (double)s[14] / (double)n;
+    if (t->wave_started_empty) t->empty_tp_frac = (double)s[1] / (double)n;
+  }
   if (e == 2) {
     set_error("predictor table reached its cap of %lld entries", (long long)t->max_entries);
     return HRPP_CAPACITY;

@@ -126,6 +126,8 @@ struct TableDev {
   bool deferred = false;
   int64_t pending = 0;
   double start_tp_frac = 1.0;  // wave-start TP fraction of the last live wave
+  double empty_tp_frac = -1.0;  // TP fraction of the last live wave that started on an empty table
+  bool wave_started_empty = false;
   int64_t fast_wcap = 0;  // fast mode: initialised wave-slot capacity
   // stream-ordered clear: every later call on the table waits for it
   cudaEvent_t clear_ev = nullptr;

@@ -37,6 +37,13 @@ namespace hrpp {
 #define HRPP_EARLY_TRACE 1
 #endif
 
+#ifndef HRPP_SORT_PRIO
+#define HRPP_SORT_PRIO 0
+#endif
+#ifndef HRPP_LEADER_FIRST
+#define HRPP_LEADER_FIRST 0
+#endif
+
 int g_live_rounds = 0;
 int g_consult_short = 32;  // segments up to this many rays are replayed by one lane
 
@@ -924,6 +931,8 @@ struct SidePool {
   cudaEvent_t fork, join[8];
   cudaEvent_t seg_ready, cls_ready;  // segment count / class bounds written
   cudaEvent_t trace_done;            // early fallback traversal finished
+  cudaStream_t hi;                   // highest priority: the grouping beside the early traversal
+  cudaEvent_t group_done;
 };
 
 static SidePool& side_pool() {
@@ -941,6 +950,10 @@ static SidePool& side_pool() {
     cudaEventCreateWithFlags(&p.seg_ready, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&p.cls_ready, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&p.trace_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p.group_done, cudaEventDisableTiming);
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    cudaStreamCreateWithPriority(&p.hi, cudaStreamNonBlocking, hi_prio);
     it = pools.emplace(dev, p).first;
   }
   return it->second;
@@ -1067,6 +1080,60 @@ __global__ void __launch_bounds__(256) k_eval0_empty(const int32_t* __restrict__
     seg_of_ray[sidx[p]] = seg_id[p] - 1;
 }
 
+// ---------------------------------------------------------------------------
+// Leader-first schedule of a live wave on an empty table (run_consult).
+// Every key segment's first ray (its leader) is a NEG and needs its full
+// traversal; if it hits, anc[leaf] is the entry's first node for every later
+// ray of the key.  A later ray that hits that node is a TP at its turn
+// whatever else the wave appends (entries only grow), so it never needs a
+// full traversal; only the rays that miss it are traced.  The replay then
+// runs as usual from the stored states (applied = 1).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mark_leaders(ConsultArgs a) {
+  const int ns = *a.nsegs;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
+       s += (int64_t)gridDim.x * blockDim.x)
+    a.need[a.sidx[a.seg_start[s]]] = 1;
+}
+
+template <bool CLOSEST, int STACK>
+__global__ void __launch_bounds__(HRPP_EVAL_BS, HRPP_EVAL_MINB * 128 / HRPP_EVAL_BS)
+    k_follow(ConsultArgs a, int64_t n) {
+  if (*a.err) return;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = a.sidx[p];
+    const int32_t s = a.seg_id[p] - 1;
+    const int32_t lead = a.sidx[a.seg_start[s]];
+    Hit acc = empty_entry_result(CLOSEST);
+    int32_t applied = 0;
+    uint8_t need = 0;
+    if (i != lead) {
+      if (a.f_found[lead]) {
+        const Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
+        fold_entry<CLOSEST>(acc, trace_from<CLOSEST, STACK>(a.nodes, a.tris, r,
+                                                            a.anc[a.f_leaf[lead]]));
+        applied = 1;
+        need = !acc.found;
+      } else {
+        need = 1;  // no entry yet at this ray's turn unless an earlier ray hits: trace
+      }
+    }
+    store_state(a, i, acc, applied);
+    a.need[i] = need;
+  }
+}
+
+template <bool CLOSEST>
+static void dispatch_follow(int stack, cudaStream_t st, const ConsultArgs& a, int64_t n) {
+  const int egrid = (int)((n + HRPP_EVAL_BS - 1) / HRPP_EVAL_BS);
+  switch (stack) {
+    case 64: k_follow<CLOSEST, 64><<<egrid, HRPP_EVAL_BS, 0, st>>>(a, n); break;
+    case 256: k_follow<CLOSEST, 256><<<egrid, HRPP_EVAL_BS, 0, st>>>(a, n); break;
+    default: k_follow<CLOSEST, 512><<<egrid, HRPP_EVAL_BS, 0, st>>>(a, n); break;
+  }
+}
+
 template <bool CLOSEST>
 static void dispatch_eval0(int stack, int grid, cudaStream_t st, const ConsultArgs& a, int64_t n,
                            int mark, bool empty_table = false) {
@@ -1130,8 +1197,21 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   // wave-start TPs (under 5 %): the early traversal then also traces those
   // few TPs (their outputs are overwritten by the entry result), a small
   // waste against the overlap won.
+  // Leader-first (k_follow): on an empty table, when this table's last
+  // empty-table live wave ended with enough TPs to pay for the extra pass
+  // (no history: closest-hit tables only).  HRPP_LEADER_FIRST=0/1/2: never,
+  // by history (default), always.  Only the schedule changes, never a result.
+  static const int leader_mode = [] {
+    const char* e = getenv("HRPP_LEADER_FIRST");
+    return e ? atoi(e) : HRPP_LEADER_FIRST;
+  }();
+  const bool leader_first =
+      c.live && rounds0 == 0 && t.n_entries == 0 &&
+      (leader_mode == 2 ||
+       (leader_mode == 1 && (t.empty_tp_frac < 0.0 ? t.closest : t.empty_tp_frac >= 0.25)));
+  t.wave_started_empty = t.n_entries == 0;
   const bool early_trace =
-      c.live && rounds0 == 0 &&
+      c.live && rounds0 == 0 && !leader_first &&
       (HRPP_EARLY_TRACE == 2 ||
        (HRPP_EARLY_TRACE == 1 && (t.n_entries == 0 || t.start_tp_frac < 0.05)));
   if (early_trace) {
@@ -1157,9 +1237,25 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
       return rc;
     HRPP_CK(cudaEventRecord(sp.trace_done, sp.s[0]));
   }
-  if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st,
-                         reinterpret_cast<int*>(pin + 32), prepacked)))
+  static const int sort_prio = [] {
+    const char* e = getenv("HRPP_SORT_PRIO");
+    return e ? atoi(e) : HRPP_SORT_PRIO;
+  }();
+  if (early_trace && sort_prio) {
+    // The traversal's one-warp blocks fill every SM, so a grouping queued at
+    // the same priority only runs in the traversal's tail; at the highest
+    // priority its blocks take the slots the traversal's blocks free.
+    SidePool& sp = side_pool();
+    HRPP_CK(cudaStreamWaitEvent(sp.hi, sp.fork, 0));
+    if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, sp.hi,
+                           reinterpret_cast<int*>(pin + 32), prepacked)))
+      return rc;
+    HRPP_CK(cudaEventRecord(sp.group_done, sp.hi));
+    HRPP_CK(cudaStreamWaitEvent(st, sp.group_done, 0));
+  } else if ((rc = group_by_key(t.ws, keys, n, 1 + 2 * t.precision, &seg, st,
+                                reinterpret_cast<int*>(pin + 32), prepacked))) {
     return rc;
+  }
   ConsultArgs a{};
   Workspace& ws = t.ws;
   if ((rc = ws.get("k_segofray", n, &a.seg_of_ray))) return rc;
@@ -1226,7 +1322,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
   }
   const int rounds = g_live_rounds < 0 ? 0 : g_live_rounds;
   // suspend/resume rounds store states for every ray; the default path does not
-  a.sparse_state = !(c.live && rounds > 0);
+  a.sparse_state = !(c.live && (rounds > 0 || leader_first));
   if (c.live) {
     // The fallback traversal writes the wave's outputs directly (a ray that
     // turns out a TP is overwritten by its entry result later; every other
@@ -1253,9 +1349,17 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.f_known_clear = nullptr;
     if (!early_trace) {  // (the early traversal writes known = 1 for every ray)
       HRPP_CK(cudaMemsetAsync(f_known, 0, n, st));
-      HRPP_CK(cudaMemsetAsync(a.need, rounds > 0 ? 0 : 1, n, st));  // eval0 clears the TPs
+      // eval0 clears the TPs; leader-first marks the leaders
+      HRPP_CK(cudaMemsetAsync(a.need, rounds > 0 || leader_first ? 0 : 1, n, st));
     }
-    {
+    if (leader_first) {
+      ProfScope ps(P_CONSULT, st);
+      k_eval0_empty<<<grid_for(n, 256, num_sms() * 16), 256, 0, st>>>(a.sidx, a.seg_id, n,
+                                                                      a.seg_of_ray);
+      HRPP_LAUNCHED();
+      k_mark_leaders<<<grid_for(n, 256, num_sms() * 8), 256, 0, st>>>(a);
+      HRPP_LAUNCHED();
+    } else {
       ProfScope ps(P_CONSULT, st);
       if (t.closest) dispatch_eval0<true>(b.stack, grid, st, a, n, rounds == 0, t.n_entries == 0);
       else dispatch_eval0<false>(b.stack, grid, st, a, n, rounds == 0, t.n_entries == 0);
@@ -1282,6 +1386,16 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     // wave-start entry; trace them, then one replay completes the wave.
     // rounds > 0: exact replay rounds, the last one speculative.
     if (rounds > 0 && (rc = resolve_nsegs())) return rc;  // the replay rounds use LL
+    if (leader_first) {  // trace the leaders, then evaluate their node for the followers
+      if ((rc = compact_flags(ws, a.need, n, queue, qcount, st))) return rc;
+      if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, queue, qcount, to,
+                             err, st, &ws)))
+        return rc;
+      ProfScope ps(P_CONSULT, st);
+      if (t.closest) dispatch_follow<true>(b.stack, st, a, n);
+      else dispatch_follow<false>(b.stack, st, a, n);
+      HRPP_LAUNCHED();
+    }
     for (int r = rounds == 0 ? rounds : 0; r <= rounds && !early_trace; r++) {
       if (rounds > 0) {
         a.spec = r == rounds ? 2 : 0;

@@ -11,7 +11,8 @@ import bench  # noqa: E402
 import paper_1910_01304_b200 as hb  # noqa: E402
 
 TL = "--timeline" in sys.argv
-sys.argv = [a for a in sys.argv if a != "--timeline"]
+MODE = "fast" if "--fast" in sys.argv else "live"
+sys.argv = [a for a in sys.argv if a not in ("--timeline", "--fast")]
 args = bench.parse()
 sc, bvh, waves = bench.make_workload_device(args)
 dw = [(w[2], *w[3:]) for w in waves]
@@ -24,7 +25,7 @@ def frame():
     for t in tables.values():
         t.clear()
     for closest, O, D, t0, t1 in dw:
-        hb.trace_wave(bvh, tables[closest], "live", O, D, t0, t1, closest)
+        hb.trace_wave(bvh, tables[closest], MODE, O, D, t0, t1, closest)
 
 
 for _ in range(3):
