@@ -448,7 +448,7 @@ def run_ours(args, rank, world, local_rank):
     alg = {  # algorithmic bytes per frame
         "hash": 32 * n_local,
         "trace_queue": 64 * n_fallback + 32 * s_live[4] + 36 * s_live[5],
-        "consult": 72 * n_local + 36 * s_live[6] + 36 * s_live[7] + 32 * stored_live,
+        "consult": 72 * n_local + 32 * s_live[6] + 36 * s_live[7] + 32 * stored_live,
     }
     peak = (json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
             if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0)
@@ -462,6 +462,7 @@ def run_ours(args, rank, world, local_rank):
                "share": round(ms / (ms_live / steps), 4)}
         if k in alg and ms > 0:
             ent["achieved_gbs"] = round(alg[k] / (ms * 1e-3) / 1e9, 2)
+            ent["frac_of_hbm_peak"] = round(alg[k] / (ms * 1e-3) / 1e9 / peak, 4)
         stages[k] = ent
     dom = dom_stage
     tq = prof_timed[dom]  # (ms, launches) of the dominant stage inside the timed region
