@@ -266,6 +266,17 @@ __device__ __forceinline__ bool box_hit_s(const NodeBox& n, double ox, double oy
   return tn <= tf;
 }
 
+// HRPP_TRI_PREFETCH: 1 = on entering a leaf, prefetch the records of its
+// later triangles into L1 (the loop tests them one after the other, each a
+// dependent 96-B load); 2 = also prefetch the first record as soon as a leaf
+// node is loaded, before its box test is decided.  (Measured: DESIGN.md 12.)
+#ifndef HRPP_TRI_PREFETCH
+#define HRPP_TRI_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // Triangle v0 and edges e1, e2 in float64 (the reference's values).
 __device__ __forceinline__ void load_tri(const DTri* __restrict__ tris, int32_t k, double v[9]) {
 #if HRPP_NODE_F64
@@ -516,6 +527,12 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
     h.boxes++;
 #if HRPP_BOX32
     const NodeBox32 nb = load_node32(nodes, nd);
+#if HRPP_TRI_PREFETCH >= 2
+    if (nb.a < 0) {
+      prefetch_l1(tris + ~nb.a);
+      prefetch_l1(reinterpret_cast<const char*>(tris + ~nb.a) + 64);
+    }
+#endif
     if (box_hit32(nb, r, ivneg, t1f, h.t)) {
 #else
     const NodeBox nb = load_node(nodes, nd);
@@ -532,6 +549,13 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         continue;
       }
       const int32_t f = ~a, e = f + b;
+#if HRPP_TRI_PREFETCH >= 1
+      {  // records f+1 .. e-1: 96 B each, consecutive
+        const char* q = reinterpret_cast<const char*>(tris + f) + 96;
+        const char* qe = reinterpret_cast<const char*>(tris + e);
+        for (; q < qe; q += 128) prefetch_l1(q);
+      }
+#endif
 #pragma unroll 1
       for (int32_t k = f; k < e; k++) {
         double t, u, v;
