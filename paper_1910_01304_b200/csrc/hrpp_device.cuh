@@ -750,6 +750,109 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
 }
 #endif  // HRPP_PAIRS
 
+// HRPP_LEAF_BATCH = R > 0: the full-traversal kernel runs trace_warp, a
+// warp-synchronous form of the same per-ray loop in which a lane that
+// reaches a leaf waits ("parks") until R * parked >= walking lanes, and the
+// parked lanes then test their triangles together.  Each ray still performs
+// exactly its own sequence of box and triangle tests (a parked ray does
+// nothing in between), so results and counts are the reference's; only the
+// interleaving between the rays of a warp changes.  On BVHs whose triangles
+// are far smaller than a ray's footprint a ray tests 60-90 boxes per 2-3
+// triangles, so without this about one lane per iteration runs the ~95
+// instruction triangle test alone (profiles/r2b_c5_trace_regions.md).
+#ifndef HRPP_LEAF_BATCH
+#define HRPP_LEAF_BATCH 0
+#endif
+#if HRPP_LEAF_BATCH && HRPP_BOX32 && !HRPP_PAIRS
+template <bool CLOSEST, typename Stack>
+__device__ __forceinline__ Hit trace_warp(const DNode* __restrict__ nodes,
+                                          const DTri* __restrict__ tris, const Ray& r,
+                                          int32_t start, Stack& stack, bool valid) {
+  // every lane of the warp must call this (valid = false: no ray)
+  int top = 0;
+  int32_t nd = start;
+  uint32_t ivneg = (r.ivx < 0.0f ? 1u : 0u) | (r.ivy < 0.0f ? 2u : 0u) |
+                   (r.ivz < 0.0f ? 4u : 0u) | (r.dx >= 0.0f ? 0u : 8u) |
+                   (r.dy >= 0.0f ? 0u : 16u) | (r.dz >= 0.0f ? 0u : 32u);
+#if HRPP_OPAQUE_SIGNS
+  asm volatile("mov.u32 %0, %0;" : "+r"(ivneg));
+#endif
+  const uint32_t dmask = (ivneg & 0x38u) << 24;
+  Hit h;
+  h.t = r.tmax;
+  h.slot = -1;
+  h.boxes = 0;
+  h.tris = 0;
+  float t1f = (float)h.t;
+  int state = valid ? 0 : 2;  // 0 walking, 1 parked at a leaf, 2 finished
+  int32_t lf = 0, le = 0;     // the parked leaf's slots
+  for (;;) {
+    if (state == 0) {
+      h.boxes++;
+      const NodeBox32 nb = load_node32(nodes, nd);
+      bool pop = true;
+      if (box_hit32(nb, r, ivneg, t1f, h.t)) {
+        if (nb.a >= 0) {
+          const int32_t right = nb.b & 0x07FFFFFF;
+          const bool go_right = ((uint32_t)nb.b & dmask) != 0u;
+          stack[top++] = go_right ? nb.a : right;  // far
+          nd = go_right ? right : nb.a;            // near, visited next
+          pop = false;
+        } else if (nb.b > 0) {
+          lf = ~nb.a;
+          le = lf + nb.b;
+          state = 1;
+          pop = false;
+        }
+      }
+      if (pop) {
+        if (top == 0) state = 2;
+        else nd = stack[--top];
+      }
+    }
+    // parked lanes in the high half, walking lanes in the low half
+    const unsigned cnt =
+        __reduce_add_sync(0xffffffffu, state == 1 ? 0x10000u : (state == 0 ? 1u : 0u));
+    const unsigned np = cnt >> 16, nw = cnt & 0xffffu;
+    if (np == 0) {
+      if (nw == 0) break;
+      continue;
+    }
+    if (np * (unsigned)HRPP_LEAF_BATCH < nw) continue;
+    if (state == 1) {
+#pragma unroll 1
+      for (int32_t k = lf; k < le; k++) {
+        double t, u, v;
+        h.tris++;
+        float fo[3] = {r.ox, r.oy, r.oz}, fd[3] = {r.dx, r.dy, r.dz};
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          asm volatile("mov.b32 %0, %0;" : "+f"(fo[c]));
+          asm volatile("mov.b32 %0, %0;" : "+f"(fd[c]));
+        }
+        if (tri_test(tris, k, fo[0], fo[1], fo[2], fd[0], fd[1], fd[2], t, u, v) &&
+            t >= r.tmin && (h.slot < 0 ? t <= h.t : t < h.t)) {
+          h.t = t;
+          t1f = (float)t;
+          h.slot = k;
+          if (!CLOSEST) break;
+        }
+      }
+      if (!CLOSEST && h.slot >= 0) state = 2;
+      else if (top == 0) state = 2;
+      else {
+        nd = stack[--top];
+        state = 0;
+      }
+    }
+  }
+  h.found = h.slot >= 0;
+  if (!CLOSEST && !h.found) h.t = 0.0;
+  h.leaf = h.found ? slot_leaf(tris, h.slot) : -1;
+  return h;
+}
+#endif
+
 template <bool CLOSEST, int STACK>
 __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,
                                           const DTri* __restrict__ tris, const Ray& r,
