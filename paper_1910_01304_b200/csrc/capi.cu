@@ -56,7 +56,7 @@ int Workspace::get_raw(const char* name, size_t bytes, void** out) {
 }
 
 BvhDev::~BvhDev() {
-  cudaFree(nodes_base ? nodes_base : (void*)nodes);
+  cudaFree(nodes);
   cudaFree(tris);
   cudaFree(depth);
   for (auto& kv : anc) cudaFree(kv.second);
@@ -474,40 +474,7 @@ int hrpp_bvh_create(const float* bmin, const float* bmax, const int32_t* left,
     h->root_lo[k] = bmin[k];
     h->root_hi[k] = bmax[k];
   }
-#if HRPP_PAIRS
-  // child-pair records, below the node array: pair(i) = ((DPair*)nodes)[-1 - i]
-  // (interior nodes only; the slots of leaves are never read)
-  static_assert(sizeof(DPair) == 64 && sizeof(DNode) == 32, "record sizes");
-  bool ok = cudaMalloc(&h->nodes_base, (sizeof(DPair) + sizeof(DNode)) * n_nodes) == cudaSuccess;
-  if (ok) {
-    h->nodes = reinterpret_cast<DNode*>(static_cast<char*>(h->nodes_base) +
-                                        sizeof(DPair) * n_nodes);
-    std::vector<DPair> hp(n_nodes);
-    memset(hp.data(), 0, sizeof(DPair) * n_nodes);
-    for (int64_t i = 0; i < n_nodes; i++) {
-      if (left[i] < 0) continue;
-      DPair& p = hp[n_nodes - 1 - i];
-      const int32_t L = left[i], R = right[i];
-      const bool ll = left[L] < 0, rl = left[R] < 0;
-      const int ax = axis[i] == 1 ? 1 : (axis[i] == 2 ? 2 : 0);
-      for (int k = 0; k < 3; k++) {
-        p.llo[k] = bmin[3 * L + k];
-        p.lhi[k] = bmax[3 * L + k];
-        p.rlo[k] = bmin[3 * R + k];
-        p.rhi[k] = bmax[3 * R + k];
-      }
-      p.lid = L | (ll ? kLeafBit : 0);
-      p.laux = ll ? pack_leaf_aux(first[L], count[L]) : 0;
-      p.rid = (int32_t)((uint32_t)R | (1u << (27 + ax)) | (rl ? (uint32_t)kLeafBit : 0u));
-      p.raux = rl ? pack_leaf_aux(first[R], count[R]) : 0;
-    }
-    ok = cudaMemcpy(h->nodes_base, hp.data(), sizeof(DPair) * n_nodes, cudaMemcpyHostToDevice) ==
-         cudaSuccess;
-  }
-  ok = ok &&
-#else
   bool ok = cudaMalloc(&h->nodes, sizeof(DNode) * n_nodes) == cudaSuccess &&
-#endif
             cudaMalloc(&h->tris, sizeof(DTri) * ht.size()) == cudaSuccess &&
             cudaMalloc(&h->depth, sizeof(int32_t) * n_nodes) == cudaSuccess &&
             cudaMemcpy(h->nodes, hn.data(), sizeof(DNode) * n_nodes, cudaMemcpyHostToDevice) ==

@@ -79,35 +79,6 @@ struct __align__(16) DTri {  // 48 B: three 16-B loads
 };
 #endif
 
-// HRPP_PAIRS (default 0; measured slower): interior nodes also have a 64-B child-pair record
-// holding both children's boxes, so entering a node costs one dependent load
-// for two box tests and a popped far child needs no load for its test
-// (trace_stk below).  pair(i) lives at ((DPair*)nodes)[-1 - i]: the pair
-// array is allocated directly below the node array, so every kernel
-// addresses both through its one `nodes` pointer.
-#ifndef HRPP_PAIRS
-#define HRPP_PAIRS 0
-#endif
-#if HRPP_PAIRS && !HRPP_BOX32
-#error "HRPP_PAIRS needs the float32 slab test (HRPP_BOX32)"
-#endif
-constexpr int32_t kIdMask = 0x07FFFFFF;   // node ids are < 2^27
-constexpr int32_t kLeafBit = 1 << 30;     // child word: the child is a leaf
-struct __align__(64) DPair {  // two 256-bit loads
-  float llo[3];
-  int32_t lid;   // left child id | kLeafBit
-  float lhi[3];
-  int32_t laux;  // leaf child: first | count << 27 (count <= 15), else -1; interior: 0
-  float rlo[3];
-  int32_t rid;   // right child id | 1 << (27 + axis) | kLeafBit
-  float rhi[3];
-  int32_t raux;
-};
-
-__host__ __device__ inline int32_t pack_leaf_aux(int32_t first, int32_t count) {
-  return (count <= 15 && first >= 0 && first <= kIdMask) ? (first | (count << 27)) : -1;
-}
-
 // Host-side packing of the reference's arrays into the device records.
 __host__ __device__ inline void pack_node(DNode& d, const float* lo, const float* hi, int32_t a,
                                           int32_t b) {
@@ -264,17 +235,6 @@ __device__ __forceinline__ bool box_hit_s(const NodeBox& n, double ox, double oy
   if (a > tn) tn = a;
   if (b < tf) tf = b;
   return tn <= tf;
-}
-
-// HRPP_TRI_PREFETCH: 1 = on entering a leaf, prefetch the records of its
-// later triangles into L1 (the loop tests them one after the other, each a
-// dependent 96-B load); 2 = also prefetch the first record as soon as a leaf
-// node is loaded, before its box test is decided.  (Measured: DESIGN.md 12.)
-#ifndef HRPP_TRI_PREFETCH
-#define HRPP_TRI_PREFETCH 0
-#endif
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
 // Triangle v0 and edges e1, e2 in float64 (the reference's values).
@@ -474,7 +434,6 @@ struct LocalStack {
   __device__ __forceinline__ int32_t& operator[](int i) { return s[i]; }
 };
 
-#if !HRPP_PAIRS
 // trace_closest / trace_any from `start` (hrpp/kernels.py:89-206).
 // Traversal order: pop, count visit + box test, leaf = slots [first,
 // first+count) in order, interior pushes far then near (near = left iff
@@ -527,12 +486,6 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
     h.boxes++;
 #if HRPP_BOX32
     const NodeBox32 nb = load_node32(nodes, nd);
-#if HRPP_TRI_PREFETCH >= 2
-    if (nb.a < 0) {
-      prefetch_l1(tris + ~nb.a);
-      prefetch_l1(reinterpret_cast<const char*>(tris + ~nb.a) + 64);
-    }
-#endif
     if (box_hit32(nb, r, ivneg, t1f, h.t)) {
 #else
     const NodeBox nb = load_node(nodes, nd);
@@ -549,13 +502,6 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
         continue;
       }
       const int32_t f = ~a, e = f + b;
-#if HRPP_TRI_PREFETCH >= 1
-      {  // records f+1 .. e-1: 96 B each, consecutive
-        const char* q = reinterpret_cast<const char*>(tris + f) + 96;
-        const char* qe = reinterpret_cast<const char*>(tris + e);
-        for (; q < qe; q += 128) prefetch_l1(q);
-      }
-#endif
 #pragma unroll 1
       for (int32_t k = f; k < e; k++) {
         double t, u, v;
@@ -596,262 +542,6 @@ __device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
   h.leaf = h.found ? slot_leaf(tris, h.slot) : -1;
   return h;
 }
-#else  // HRPP_PAIRS
-
-struct PairBox {
-  NodeBox32 l, r;  // a = child word, b = aux
-};
-
-__device__ __forceinline__ PairBox load_pair(const DNode* __restrict__ nodes, int32_t nd) {
-  const DPair* p = reinterpret_cast<const DPair*>(nodes) - 1 - nd;
-  PairBox q;
-  float a0, b0, a1, b1;
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=f"(q.l.lx), "=f"(q.l.ly), "=f"(q.l.lz), "=f"(a0), "=f"(q.l.hx), "=f"(q.l.hy),
-        "=f"(q.l.hz), "=f"(b0)
-      : "l"(p));
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8+32];"
-      : "=f"(q.r.lx), "=f"(q.r.ly), "=f"(q.r.lz), "=f"(a1), "=f"(q.r.hx), "=f"(q.r.hy),
-        "=f"(q.r.hz), "=f"(b1)
-      : "l"(p));
-  q.l.a = __float_as_int(a0);
-  q.l.b = __float_as_int(b0);
-  q.r.a = __float_as_int(a1);
-  q.r.b = __float_as_int(b1);
-  return q;
-}
-
-// trace_closest / trace_any from `start` (hrpp/kernels.py:89-206), the same
-// visits, tests and counts as the reference's loop (pop, count visit + box
-// test, leaf = slots [first, first+count) in order, interior pushes far then
-// near; near = left iff d[axis] >= 0), restructured around child-pair
-// records so that a ray makes one dependent load per ENTERED interior node
-// instead of one per popped node:
-//  * entering a node loads both children's boxes (one 64-B record) and
-//    tests both.  The near child is the next pop, so its test is the
-//    reference's (same interval).  The far child's test belongs to its pop:
-//    the slab test is monotone in the interval end, so a miss now is a miss
-//    then; a hit now is a hit then unless the interval shrank in between.
-//  * closest hit: a far child that misses now is only counted (every pushed
-//    node is popped eventually, so the count is the same); one that hits is
-//    pushed, and re-tested at its pop against its own box only if a closer
-//    hit was found since (entries below `stale_top`).
-//  * any hit: the interval never changes before the traversal ends, so the
-//    far test is final; a miss is pushed as a marker (-1) and counted at its
-//    pop, because the first hit ends the loop with the stack unpopped.
-//  * a near leaf's slot range comes with the pair record (aux), so a leaf
-//    reached as near child needs no node load at all.
-template <bool CLOSEST, typename Stack>
-__device__ __forceinline__ Hit trace_stk(const DNode* __restrict__ nodes,
-                                         const DTri* __restrict__ tris, const Ray& r,
-                                         int32_t start, Stack& stack) {
-  int top = 0;
-  int stale_top = 0;  // closest: entries [0, stale_top) were tested before the last closer hit
-  // bits 0-2: 1/d < 0 per axis; bits 3-5: d < 0 (near child right)
-  uint32_t ivneg = (r.ivx < 0.0f ? 1u : 0u) | (r.ivy < 0.0f ? 2u : 0u) |
-                   (r.ivz < 0.0f ? 4u : 0u) | (r.dx >= 0.0f ? 0u : 8u) |
-                   (r.dy >= 0.0f ? 0u : 16u) | (r.dz >= 0.0f ? 0u : 32u);
-#if HRPP_OPAQUE_SIGNS
-  asm volatile("mov.u32 %0, %0;" : "+r"(ivneg));
-#endif
-  const uint32_t dmask = (ivneg & 0x38u) << 24;  // d[axis] < 0 at bit 27 + axis
-  Hit h;
-  h.t = r.tmax;  // see the single-node loop above: tmax itself is not live
-  h.slot = -1;
-  h.boxes = 1;
-  h.tris = 0;
-  float t1f = (float)h.t;
-  int32_t cur = -1;          // interior node to enter (its own test passed), or -1: pop
-  int32_t lf = 0, lcnt = 0;  // leaf slots to test first in the next iteration
-  {
-    const NodeBox32 nb = load_node32(nodes, start);
-    if (box_hit32(nb, r, ivneg, t1f, h.t)) {
-      if (nb.a >= 0) cur = start;
-      else { lf = ~nb.a; lcnt = nb.b; }
-    }
-  }
-  for (;;) {
-    if (lcnt > 0) {
-      const int32_t e = lf + lcnt;
-      lcnt = 0;
-#pragma unroll 1
-      for (int32_t k = lf; k < e; k++) {
-        double t, u, v;
-        h.tris++;
-        float fo[3] = {r.ox, r.oy, r.oz}, fd[3] = {r.dx, r.dy, r.dz};
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          asm volatile("mov.b32 %0, %0;" : "+f"(fo[c]));
-          asm volatile("mov.b32 %0, %0;" : "+f"(fd[c]));
-        }
-        if (tri_test(tris, k, fo[0], fo[1], fo[2], fd[0], fd[1], fd[2], t, u, v) &&
-            t >= r.tmin && (h.slot < 0 ? t <= h.t : t < h.t)) {
-          h.t = t;
-          t1f = (float)t;
-          h.slot = k;
-          if (CLOSEST) stale_top = top;
-          else break;
-        }
-      }
-      if (!CLOSEST && h.slot >= 0) break;
-    }
-    if (cur < 0) {
-      if (top == 0) break;
-      const int32_t e = stack[--top];
-      h.boxes++;
-      if (!CLOSEST && e < 0) continue;  // a far child that missed when it was pushed
-      const bool stale = CLOSEST && top < stale_top;
-      if (stale) stale_top = top;
-      const bool leaf = (e & kLeafBit) != 0;
-      const int32_t id = e & kIdMask;
-      if (stale || leaf) {
-        const NodeBox32 nb = load_node32(nodes, id);
-        if (stale && !box_hit32(nb, r, ivneg, t1f, h.t)) continue;
-        if (leaf) {
-          lf = ~nb.a;
-          lcnt = nb.b;
-          continue;
-        }
-      }
-      cur = id;
-    }
-    const PairBox pb = load_pair(nodes, cur);
-    const bool hl = box_hit32(pb.l, r, ivneg, t1f, h.t);
-    const bool hr = box_hit32(pb.r, r, ivneg, t1f, h.t);
-    const bool go_right = ((uint32_t)pb.r.a & dmask) != 0u;
-    const bool hn = go_right ? hr : hl, hf = go_right ? hl : hr;
-    const int32_t nw = go_right ? pb.r.a : pb.l.a, naux = go_right ? pb.r.b : pb.l.b;
-    const int32_t fw = (go_right ? pb.l.a : pb.r.a) & (kIdMask | kLeafBit);
-    h.boxes++;  // the near child's pop
-    if (CLOSEST) {
-      if (hf) stack[top++] = fw;
-      else h.boxes++;  // popped and rejected later: counted now
-    } else {
-      stack[top++] = hf ? fw : -1;
-    }
-    cur = -1;
-    if (hn) {
-      if (!(nw & kLeafBit)) {
-        cur = nw & kIdMask;
-      } else if (naux >= 0) {
-        lf = naux & kIdMask;
-        lcnt = naux >> 27;
-      } else {
-        const NodeBox32 nb = load_node32(nodes, nw & kIdMask);
-        lf = ~nb.a;
-        lcnt = nb.b;
-      }
-    }
-  }
-  h.found = h.slot >= 0;
-  if (!CLOSEST && !h.found) h.t = 0.0;  // trace_any's miss (hrpp/kernels.py:206)
-  h.leaf = h.found ? slot_leaf(tris, h.slot) : -1;
-  return h;
-}
-#endif  // HRPP_PAIRS
-
-// HRPP_LEAF_BATCH = R > 0: the full-traversal kernel runs trace_warp, a
-// warp-synchronous form of the same per-ray loop in which a lane that
-// reaches a leaf waits ("parks") until R * parked >= walking lanes, and the
-// parked lanes then test their triangles together.  Each ray still performs
-// exactly its own sequence of box and triangle tests (a parked ray does
-// nothing in between), so results and counts are the reference's; only the
-// interleaving between the rays of a warp changes.  On BVHs whose triangles
-// are far smaller than a ray's footprint a ray tests 60-90 boxes per 2-3
-// triangles, so without this about one lane per iteration runs the ~95
-// instruction triangle test alone (profiles/r2b_c5_trace_regions.md).
-#ifndef HRPP_LEAF_BATCH
-#define HRPP_LEAF_BATCH 0
-#endif
-#if HRPP_LEAF_BATCH && HRPP_BOX32 && !HRPP_PAIRS
-template <bool CLOSEST, typename Stack>
-__device__ __forceinline__ Hit trace_warp(const DNode* __restrict__ nodes,
-                                          const DTri* __restrict__ tris, const Ray& r,
-                                          int32_t start, Stack& stack, bool valid) {
-  // every lane of the warp must call this (valid = false: no ray)
-  int top = 0;
-  int32_t nd = start;
-  uint32_t ivneg = (r.ivx < 0.0f ? 1u : 0u) | (r.ivy < 0.0f ? 2u : 0u) |
-                   (r.ivz < 0.0f ? 4u : 0u) | (r.dx >= 0.0f ? 0u : 8u) |
-                   (r.dy >= 0.0f ? 0u : 16u) | (r.dz >= 0.0f ? 0u : 32u);
-#if HRPP_OPAQUE_SIGNS
-  asm volatile("mov.u32 %0, %0;" : "+r"(ivneg));
-#endif
-  const uint32_t dmask = (ivneg & 0x38u) << 24;
-  Hit h;
-  h.t = r.tmax;
-  h.slot = -1;
-  h.boxes = 0;
-  h.tris = 0;
-  float t1f = (float)h.t;
-  int state = valid ? 0 : 2;  // 0 walking, 1 parked at a leaf, 2 finished
-  int32_t lf = 0, le = 0;     // the parked leaf's slots
-  for (;;) {
-    if (state == 0) {
-      h.boxes++;
-      const NodeBox32 nb = load_node32(nodes, nd);
-      bool pop = true;
-      if (box_hit32(nb, r, ivneg, t1f, h.t)) {
-        if (nb.a >= 0) {
-          const int32_t right = nb.b & 0x07FFFFFF;
-          const bool go_right = ((uint32_t)nb.b & dmask) != 0u;
-          stack[top++] = go_right ? nb.a : right;  // far
-          nd = go_right ? right : nb.a;            // near, visited next
-          pop = false;
-        } else if (nb.b > 0) {
-          lf = ~nb.a;
-          le = lf + nb.b;
-          state = 1;
-          pop = false;
-        }
-      }
-      if (pop) {
-        if (top == 0) state = 2;
-        else nd = stack[--top];
-      }
-    }
-    // parked lanes in the high half, walking lanes in the low half
-    const unsigned cnt =
-        __reduce_add_sync(0xffffffffu, state == 1 ? 0x10000u : (state == 0 ? 1u : 0u));
-    const unsigned np = cnt >> 16, nw = cnt & 0xffffu;
-    if (np == 0) {
-      if (nw == 0) break;
-      continue;
-    }
-    if (np * (unsigned)HRPP_LEAF_BATCH < nw) continue;
-    if (state == 1) {
-#pragma unroll 1
-      for (int32_t k = lf; k < le; k++) {
-        double t, u, v;
-        h.tris++;
-        float fo[3] = {r.ox, r.oy, r.oz}, fd[3] = {r.dx, r.dy, r.dz};
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-          asm volatile("mov.b32 %0, %0;" : "+f"(fo[c]));
-          asm volatile("mov.b32 %0, %0;" : "+f"(fd[c]));
-        }
-        if (tri_test(tris, k, fo[0], fo[1], fo[2], fd[0], fd[1], fd[2], t, u, v) &&
-            t >= r.tmin && (h.slot < 0 ? t <= h.t : t < h.t)) {
-          h.t = t;
-          t1f = (float)t;
-          h.slot = k;
-          if (!CLOSEST) break;
-        }
-      }
-      if (!CLOSEST && h.slot >= 0) state = 2;
-      else if (top == 0) state = 2;
-      else {
-        nd = stack[--top];
-        state = 0;
-      }
-    }
-  }
-  h.found = h.slot >= 0;
-  if (!CLOSEST && !h.found) h.t = 0.0;
-  h.leaf = h.found ? slot_leaf(tris, h.slot) : -1;
-  return h;
-}
-#endif
 
 template <bool CLOSEST, int STACK>
 __device__ __forceinline__ Hit trace_from(const DNode* __restrict__ nodes,

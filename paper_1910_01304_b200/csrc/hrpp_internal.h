@@ -88,7 +88,6 @@ struct TraceOut {
 struct BvhDev {
   int device = 0;
   DNode* nodes = nullptr;
-  void* nodes_base = nullptr;  // HRPP_PAIRS: the allocation (pair records, then `nodes`)
   DTri* tris = nullptr;
   int32_t* depth = nullptr;
   int32_t* tri_ids = nullptr;

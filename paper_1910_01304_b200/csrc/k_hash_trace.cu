@@ -323,24 +323,11 @@ __global__ void __launch_bounds__(HRPP_TRACE_BS, HRPP_TRACE_MINB * 128 / HRPP_TR
   const int64_t count = a.count_dev ? (int64_t)*a.count_dev : a.n;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long sb = 0, stt = 0;
-#if HRPP_LEAF_BATCH && HRPP_BOX32 && !HRPP_PAIRS
-  // warp-synchronous traversal: every lane enters, lanes without a ray idle
-  static_assert(HRPP_TRACE_BS % 32 == 0, "whole warps");
-  const bool has_ray = q < count;
-  const int64_t i = has_ray ? (a.ray_idx ? (int64_t)a.ray_idx[q] : q) : 0;
-  Ray r{};
-  if (has_ray) r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
-  LocalStack<STACK> wstack;
-  Hit h = trace_warp<CLOSEST>(a.nodes, a.tris, r, a.start, wstack, has_ray);
-  if (has_ray) {
-    const TraceOut& o = a.out;
-#else
   if (q < count) {
     const int64_t i = a.ray_idx ? (int64_t)a.ray_idx[q] : q;
     Ray r = make_ray(a.O, a.D, a.tmin, a.tmax, i);
     Hit h = trace_from<CLOSEST, STACK>(a.nodes, a.tris, r, a.start);
     const TraceOut& o = a.out;
-#endif
     if (o.found) o.found[i] = h.found;
     if (o.t) o.t[i] = (o.zero_miss_t && !h.found) ? 0.0 : h.t;
     if (o.slot) o.slot[i] = h.slot;

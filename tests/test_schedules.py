@@ -2,9 +2,8 @@
 
 The exact consult has switches that only move work around: the
 leader-first schedule of a live wave on an empty table
-(``HRPP_LEADER_FIRST``), the grouping sort on a highest-priority stream
-beside the early traversal (``HRPP_SORT_PRIO``) and, at compile time, the
-child-pair node records (``-DHRPP_PAIRS=1``).  Each is read once per
+(``HRPP_LEADER_FIRST``) and the grouping sort on a highest-priority stream
+beside the early traversal (``HRPP_SORT_PRIO``).  Each is read once per
 process, so the parity tests that compare waves with the reference's
 goldens (hrpp/tracer.py:343-371) and with the oracle are re-run in a child
 process with the switch on.
@@ -35,10 +34,3 @@ def _rerun(env_extra):
 
 def test_leader_first_and_priority_sort_are_exact():
     _rerun({"HRPP_LEADER_FIRST": "2", "HRPP_SORT_PRIO": "1"})
-
-
-def test_child_pair_records_are_exact():
-    lib = ROOT / "exp" / "pairs" / "libhrpp_b200.so"
-    if not lib.exists():
-        pytest.skip("build it with: python -m paper_1910_01304_b200.build --variant pairs -DHRPP_PAIRS=1")
-    _rerun({"HRPP_LIB": str(lib)})
