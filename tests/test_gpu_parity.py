@@ -265,6 +265,79 @@ def test_trace_box_boundaries_vs_oracle(hb, oracle_mod, scene):
             assert np.array_equal(got[k], v, equal_nan=True), (scene, closest, k)
 
 
+def _edge_seeking_rays(b, n, seed, scale=1.0):
+    """Rays aimed at triangle vertices, at points on triangle edges and a few
+    float32 ulps to either side of them (u = 0, v = 0, u + v = 1 and u = 1
+    within rounding), from origins at every distance; a share with tiny,
+    huge or zero direction components."""
+    rng = np.random.default_rng(seed)
+    m = b.tv0.shape[0]
+    k = rng.integers(0, m, n)
+    v0, v1, v2 = (x[k].astype(np.float64) for x in (b.tv0, b.tv1, b.tv2))
+    s = rng.random((n, 1))
+    which = rng.integers(0, 6, n)
+    P = np.where((which == 0)[:, None], v0 + s * (v1 - v0),
+        np.where((which == 1)[:, None], v0 + s * (v2 - v0),
+        np.where((which == 2)[:, None], v1 + s * (v2 - v1),
+        np.where((which == 3)[:, None], v0,
+        np.where((which == 4)[:, None], v1, v2)))))
+    # a few ulps off the edge, inside or outside
+    nudge = rng.integers(-3, 4, (n, 3)) * np.abs(P) * 2.0 ** -23
+    P = P + np.where(rng.random((n, 1)) < 0.5, nudge, 0.0)
+    dist = (10.0 ** rng.uniform(-3, 2, (n, 1))) * scale
+    dirs = rng.normal(size=(n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    O = (P - dirs * dist).astype(np.float32)
+    D = (P - O.astype(np.float64))
+    unit = rng.random(n) < 0.5
+    D[unit] /= np.linalg.norm(D[unit], axis=1, keepdims=True)
+    D = D.astype(np.float32)
+    special = np.array([0.0, -0.0, 1e-30, 2.0 ** -41, 2.0 ** 41, -1e20], np.float32)
+    msk = rng.random((n, 3)) < 0.03
+    D[msk] = special[rng.integers(0, special.size, int(msk.sum()))]
+    bad = ~np.isfinite(D).all(axis=1) | ~np.isfinite(O).all(axis=1)
+    D[bad] = np.float32(1.0)
+    O[bad] = np.float32(0.0)
+    return O, D, np.zeros(n), np.full(n, np.inf)
+
+
+@pytest.mark.parametrize("scene", ["spheres", "c1", "c1x2^30", "c1x2^-30", "c1x2^45", "c1x2^-100"])
+def test_trace_triangle_boundaries_vs_oracle(hb, oracle_mod, scene):
+    """Every triangle decision is the reference's float64 Moller-Trumbore
+    (hrpp/kernels.py:54-86), also for rays through vertices and edges and a
+    few float32 ulps beside them, and on the c1 scene scaled by powers of two
+    up to the reference's |det| <= 1e-9 cut-off (2^-100: every triangle is
+    rejected): hits, t, slots, leaves and both counters equal the oracle."""
+    from oracle.oracle import OracleBvh
+    if scene.startswith("c1"):
+        from paper_1910_01304_b200 import scenes
+        sc = scenes.make_scene("c1", resolution=(32, 32))
+        b = hb.build_bvh_from_arrays(sc.v0, sc.v1, sc.v2, median_split=True)
+        kk = 1.0
+        if "x" in scene:
+            kk = 2.0 ** int(scene.split("^")[1])
+            k = np.float32(kk)
+            b = hb.Bvh(b.bmin * k, b.bmax * k, b.left, b.right, b.axis, b.first, b.count,
+                       b.parent, b.depth, b.tv0 * k, b.tv1 * k, b.tv2 * k, b.tri_ids,
+                       int(b.depth.max()))
+        ob = OracleBvh(b.bmin, b.bmax, b.left, b.right, b.axis, b.first, b.count, b.parent,
+                       b.depth, b.tv0, b.tv1, b.tv2, b.tri_ids)
+    else:
+        kk = 1.0
+        g = load_golden(f"bvh_{scene}.npz")
+        b = gbvh(hb, scene)
+        ob = OracleBvh.from_dict(g)
+    O, D, tmin, tmax = _edge_seeking_rays(b, 80_000, seed=5, scale=kk)
+    for closest in (True, False):
+        got = (hb.intersect_closest_batch if closest else hb.intersect_any_batch)(
+            b, O, D, tmin, tmax)
+        ref = ob.trace_batch(closest, O, D, tmin, tmax)
+        if scene != "c1x2^-100":  # (there the reference's |det| <= 1e-9 cut-off rejects everything)
+            assert ref["found"].sum() > 1000  # the rays do reach their triangles
+        for k, v in ref.items():
+            assert np.array_equal(got[k], v, equal_nan=True), (scene, closest, k)
+
+
 # -- the wave (limit / live / baseline) ----------------------------------------------
 
 @pytest.mark.parametrize("p,g_", SETTINGS)
