@@ -325,9 +325,12 @@ __global__ void k_first_append(ConsultArgs a, int64_t n) {
     const int32_t ex_len = a.seg_exlen[s];
     if (ex_len > 0 && a.state[i].found) continue;  // TP against the wave-start entry
     if (a.f_known && !a.f_known[i]) continue;  // (live) no full result: never a first append
-    if (!a.f_found[i]) continue;
-    // (no entry: every hit appends -- skip the leaf and ancestor reads)
-    if (ex_len == 0 || !in_list(a, a.seg_exoff[s], ex_len, a.anc[a.f_leaf[i]]))
+    // a full result's leaf is -1 exactly when nothing was found (k_trace), so
+    // the found flags need no read of their own
+    const int32_t lf = a.f_leaf[i];
+    if (lf < 0) continue;
+    // (no entry: every hit appends -- skip the ancestor read)
+    if (ex_len == 0 || !in_list(a, a.seg_exoff[s], ex_len, a.anc[lf]))
       atomicMin(a.seg_f1 + s, (int32_t)i);
   }
 }
@@ -632,8 +635,11 @@ __global__ void __launch_bounds__(HRPP_REPLAY_BS, HRPP_REPLAY_MINB * 128 / HRPP_
   // (a TP's full result may never have been computed in live mode anyway).
   int32_t cnode = -1;
   bool inL = false;
-  if (valid && (L == 0 || !acc.found) && (!LIVE || a.f_known[idx]) && a.f_found[idx]) {
-    cnode = a.anc[a.f_leaf[idx]];
+  if (valid && (L == 0 || !acc.found) && (!LIVE || !a.f_known || a.f_known[idx])) {
+    const int32_t lf = a.f_leaf[idx];  // -1: nothing found
+    if (lf >= 0) cnode = a.anc[lf];
+  }
+  if (cnode >= 0) {
     for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
   }
   // Step from append to append: the rays before the next ray that grows the
@@ -740,8 +746,11 @@ __global__ void __launch_bounds__(BS, BS == 32 ? HRPP_BLOCK32_MINB : HRPP_BLOCK_
       }
       int32_t cnode = -1;  // read only by rays that are not TPs now (see k_replay_group)
       bool inL = false;
-      if (valid && (L == 0 || !acc.found) && (!LIVE || a.f_known[idx]) && a.f_found[idx]) {
-        cnode = a.anc[a.f_leaf[idx]];
+      if (valid && (L == 0 || !acc.found) && (!LIVE || !a.f_known || a.f_known[idx])) {
+        const int32_t lf = a.f_leaf[idx];  // -1: nothing found
+        if (lf >= 0) cnode = a.anc[lf];
+      }
+      if (cnode >= 0) {
         for (int32_t j = 0; j < L; j++) inL |= entry_node(a, ex_off, ex_len, app, j) == cnode;
       }
       // append to append, as in k_replay_group
@@ -1230,7 +1239,8 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     to.leaf = c.o_leaf;
     to.box32 = f_box;
     to.tri32 = f_tri;
-    to.known = f_known;  // every ray: known = 1
+    to.known = nullptr;  // every ray is traced: the consult reads no known flags (a.f_known = nullptr)
+    (void)f_known;
     to.zero_miss_t = true;
     if ((rc = launch_trace(b, t.closest, c.O, c.D, c.tmin, c.tmax, 0, n, nullptr, nullptr, to,
                            err, sp.s[0], &t.ws, true)))
@@ -1340,7 +1350,7 @@ int run_consult(const BvhDev& b, TableDev& t, const Consult& c, const uint64_t* 
     a.f_leaf = c.o_leaf;
     a.f_box32 = f_box;
     a.f_tri32 = f_tri;
-    a.f_known = f_known;
+    a.f_known = early_trace ? nullptr : f_known;  // early traversal: every full result is known
     a.o_found = c.o_found;
     a.o_t = c.o_t;
     a.o_slot = c.o_slot;
